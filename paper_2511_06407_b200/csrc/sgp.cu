@@ -1,0 +1,757 @@
+// sgp.cu — kernels and the C ABI of libsgp.so (see include/sgp.h).
+//
+// Every batched entry point launches one CTA of SGP_NT threads per chain;
+// the CTA runs the collective building blocks of sgp_core/sgp_eval/sgp_chain.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <vector>
+
+#include "sgp_chain.cuh"
+
+extern __shared__ __align__(16) char sgp_smem[];
+
+struct sgp_model {
+    ModelDev dev;
+    double *d_phi, *d_y, *d_cw, *d_prec, *d_mean;
+    int8_t *d_ckind;
+};
+
+#define CUDA_TRY(x)                                                                  \
+    do {                                                                             \
+        cudaError_t err__ = (x);                                                     \
+        if (err__ != cudaSuccess) {                                                  \
+            fprintf(stderr, "libsgp: %s failed: %s\n", #x, cudaGetErrorString(err__)); \
+            return SGP_ECUDA;                                                        \
+        }                                                                            \
+    } while (0)
+
+static inline cudaStream_t S(void *s) { return reinterpret_cast<cudaStream_t>(s); }
+
+template <typename K>
+static int launch_prep(K kernel, size_t smem) {
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) {
+            fprintf(stderr, "libsgp: smem attribute (%zu B): %s\n", smem, cudaGetErrorString(e));
+            return SGP_ECUDA;
+        }
+    }
+    return SGP_OK;
+}
+
+static int check_launch() {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        fprintf(stderr, "libsgp: launch failed: %s\n", cudaGetErrorString(e));
+        return SGP_ECUDA;
+    }
+    return SGP_OK;
+}
+
+// ===========================================================================
+// model: design matrix assembly (FeatureCache, rrgp.py:310-344)
+
+struct FeatRow {
+    int kind;  // 0 sin basis, 1 linear, 2 ones
+    int cov;
+    double m, L;
+};
+
+__global__ void k_assemble_phi(const double *__restrict__ x, int N, int P, int ld, const FeatRow *__restrict__ rows,
+                               int Dtot, double *__restrict__ phi) {
+    const int a = blockIdx.y;
+    const FeatRow r = rows[a];
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < ld; i += gridDim.x * blockDim.x) {
+        double v = 0.0;
+        if (i < N) {
+            if (r.kind == 0) {
+                const double xv = x[(size_t)i * P + r.cov];
+                v = sin(SGP_PI * r.m * (xv + r.L) / (2.0 * r.L));
+            } else if (r.kind == 1) {
+                v = x[(size_t)i * P + r.cov];
+            } else {
+                v = 1.0;
+            }
+        }
+        phi[(size_t)a * ld + i] = v;
+    }
+}
+
+extern "C" int sgp_model_create(const sgp_model_desc *desc, sgp_model **out) {
+    if (!desc || !out) return SGP_EINVAL;
+    *out = nullptr;
+    sgp_model *m = (sgp_model *)calloc(1, sizeof(sgp_model));
+    if (!m) return SGP_ENOMEM;
+    ModelParams &mp = m->dev.mp;
+    mp.lik = desc->likelihood;
+    mp.transform = desc->transform;
+    mp.sigma = desc->intercept_variance;
+    mp.vfloor = desc->variance_floor;
+    mp.loglik_const = desc->loglik_const;
+    for (int s = 0; s < 3; ++s) {
+        mp.hpos[s] = -1;
+        mp.hfixed[s] = desc->hyper_fixed[s];
+        mp.alpha[s] = desc->prior_alpha[s];
+        mp.beta[s] = desc->prior_beta[s];
+        mp.norm[s] = desc->hyper_sampled[s] ? lgamma(mp.alpha[s]) - mp.alpha[s] * log(mp.beta[s]) : 0.0;
+    }
+    if (mp.lik == SGP_LIK_QUADRATIC) {
+        const int d = desc->quad_dim;
+        if (d < 1 || !desc->h_precision || !desc->h_mean) {
+            free(m);
+            return SGP_EINVAL;
+        }
+        mp.d = d;
+        mp.J = 0;
+        mp.N = 0;
+        mp.ld = 0;
+        mp.Dtot = 0;
+        CUDA_TRY(cudaMalloc(&m->d_prec, sizeof(double) * d * d));
+        CUDA_TRY(cudaMalloc(&m->d_mean, sizeof(double) * d));
+        CUDA_TRY(cudaMemcpy(m->d_prec, desc->h_precision, sizeof(double) * d * d, cudaMemcpyHostToDevice));
+        CUDA_TRY(cudaMemcpy(m->d_mean, desc->h_mean, sizeof(double) * d, cudaMemcpyHostToDevice));
+        std::vector<int8_t> ck(d, CK_HYPER);
+        CUDA_TRY(cudaMalloc(&m->d_ckind, d));
+        CUDA_TRY(cudaMemcpy(m->d_ckind, ck.data(), d, cudaMemcpyHostToDevice));
+        m->dev.prec = m->d_prec;
+        m->dev.mean = m->d_mean;
+        m->dev.ckind = m->d_ckind;
+        *out = m;
+        return SGP_OK;
+    }
+    const int J = desc->n_functions;
+    if (J < 1 || J > 2 || desc->n_rows < 1 || desc->n_cols < 1) {
+        free(m);
+        return SGP_EINVAL;
+    }
+    mp.J = J;
+    mp.N = desc->n_rows;
+    mp.ld = (mp.N + 31) & ~31;
+    std::vector<FeatRow> rows;
+    std::vector<int8_t> ck;
+    std::vector<double> cw;
+    int pos = 0;
+    for (int j = 0; j < J; ++j) {
+        mp.fstart[j] = pos;
+        for (int k = 0; k < desc->n_kernels[j]; ++k) {
+            const sgp_kernel_desc &kd = desc->kernels[j][k];
+            if (kd.covariate < 0 || kd.covariate >= desc->n_cols) {
+                free(m);
+                return SGP_EINVAL;
+            }
+            if (kd.kind == SGP_KERNEL_GAUSSIAN) {
+                for (int mm = 1; mm <= kd.features; ++mm) {
+                    rows.push_back({0, kd.covariate, (double)mm, kd.half_width});
+                    ck.push_back(CK_GAUSS);
+                    const double t = SGP_PI * (double)mm / (2.0 * kd.half_width);
+                    cw.push_back(t * t / 4.0);
+                    mp.n_gauss++;
+                }
+            } else {
+                rows.push_back({1, kd.covariate, 0.0, 0.0});
+                ck.push_back(CK_LIN);
+                cw.push_back(0.0);
+                mp.n_lin++;
+            }
+            pos += (kd.kind == SGP_KERNEL_GAUSSIAN) ? kd.features : 1;
+        }
+        rows.push_back({2, 0, 0.0, 0.0});
+        ck.push_back(CK_INTERCEPT);
+        cw.push_back(0.0);
+        ++pos;
+        mp.D[j] = pos - mp.fstart[j];
+    }
+    if (J == 1) {
+        mp.D[1] = 0;
+        mp.fstart[1] = pos;
+    }
+    mp.Dtot = pos;
+    for (int s = 0; s < 3; ++s) {
+        if (desc->hyper_sampled[s]) {
+            mp.hpos[s] = pos++;
+            ck.push_back(CK_HYPER);
+            cw.push_back(0.0);
+        }
+    }
+    mp.d = pos;
+    const int Dt = mp.Dtot, N = mp.N, P = desc->n_cols, ld = mp.ld;
+    double *d_x = nullptr;
+    FeatRow *d_rows = nullptr;
+    CUDA_TRY(cudaMalloc(&d_x, sizeof(double) * (size_t)N * P));
+    CUDA_TRY(cudaMalloc(&d_rows, sizeof(FeatRow) * Dt));
+    CUDA_TRY(cudaMalloc(&m->d_phi, sizeof(double) * (size_t)Dt * ld));
+    CUDA_TRY(cudaMalloc(&m->d_y, sizeof(double) * ld));
+    CUDA_TRY(cudaMalloc(&m->d_ckind, mp.d));
+    CUDA_TRY(cudaMalloc(&m->d_cw, sizeof(double) * mp.d));
+    CUDA_TRY(cudaMemcpy(d_x, desc->h_x, sizeof(double) * (size_t)N * P, cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(d_rows, rows.data(), sizeof(FeatRow) * Dt, cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemset(m->d_y, 0, sizeof(double) * ld));
+    CUDA_TRY(cudaMemcpy(m->d_y, desc->h_y, sizeof(double) * N, cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(m->d_ckind, ck.data(), mp.d, cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(m->d_cw, cw.data(), sizeof(double) * mp.d, cudaMemcpyHostToDevice));
+    dim3 grid((ld + 255) / 256, Dt);
+    k_assemble_phi<<<grid, 256>>>(d_x, N, P, ld, d_rows, Dt, m->d_phi);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaDeviceSynchronize());
+    cudaFree(d_x);
+    cudaFree(d_rows);
+    m->dev.phi = m->d_phi;
+    m->dev.y = m->d_y;
+    m->dev.ckind = m->d_ckind;
+    m->dev.cw = m->d_cw;
+    *out = m;
+    return SGP_OK;
+}
+
+extern "C" int sgp_model_destroy(sgp_model *m) {
+    if (!m) return SGP_OK;
+    cudaFree(m->d_phi);
+    cudaFree(m->d_y);
+    cudaFree(m->d_cw);
+    cudaFree(m->d_ckind);
+    cudaFree(m->d_prec);
+    cudaFree(m->d_mean);
+    free(m);
+    return SGP_OK;
+}
+
+extern "C" int sgp_model_dim(const sgp_model *m) { return m ? m->dev.mp.d : SGP_EINVAL; }
+extern "C" int sgp_model_rows(const sgp_model *m) { return m ? m->dev.mp.N : SGP_EINVAL; }
+extern "C" int sgp_model_features(const sgp_model *m, int j) {
+    if (!m || j < 0 || j >= m->dev.mp.J) return SGP_EINVAL;
+    return m->dev.mp.D[j];
+}
+extern "C" size_t sgp_scratch_doubles(const sgp_model *m) {
+    return m ? sgp_scratch_per_chain(m->dev.mp.ld, m->dev.mp.d) : 0;
+}
+
+__global__ void k_phi_out(const double *phi, int ld, int N, int a0, int Dj, double *out) {
+    for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < N * Dj; idx += gridDim.x * blockDim.x) {
+        const int i = idx / Dj, a = idx - i * Dj;
+        out[idx] = phi[(size_t)(a0 + a) * ld + i];
+    }
+}
+
+extern "C" int sgp_model_phi(const sgp_model *m, int j, double *d_out, void *stream) {
+    if (!m || j < 0 || j >= m->dev.mp.J || !d_out) return SGP_EINVAL;
+    const ModelParams &mp = m->dev.mp;
+    const int a0 = j == 0 ? 0 : mp.D[0];
+    const int n = mp.N * mp.D[j];
+    k_phi_out<<<(n + 255) / 256, 256, 0, S(stream)>>>(m->dev.phi, mp.ld, mp.N, a0, mp.D[j], d_out);
+    return check_launch();
+}
+
+// ===========================================================================
+// posterior evaluation
+
+__global__ void __launch_bounds__(SGP_NT) k_eval(ModelDev M, SmemPlan pl, const double *tau, const double *q, int what,
+                                                 double *pot, double *grad, double *hess, double *sumpot, int *status,
+                                                 double *scratch, size_t spc) {
+    const int z = blockIdx.x;
+    const int d = M.mp.d;
+    ChainWS w;
+    EvalCtx E;
+    setup_ws(w, E, sgp_smem, pl, M, scratch + (size_t)z * spc);
+    for (int j = threadIdx.x; j < d; j += SGP_NT) w.q0[j] = q[(size_t)z * d + j];
+    __syncthreads();
+    double *H = hess ? hess + (size_t)z * d * d : w.H;
+    EvalOut o;
+    eval_state(E, w.q0, tau[z], what, w.grad, H, o);
+    if (grad)
+        for (int j = threadIdx.x; j < d; j += SGP_NT) grad[(size_t)z * d + j] = w.grad[j];
+    if (threadIdx.x == 0) {
+        if (pot) pot[z] = o.pot;
+        if (sumpot) sumpot[z] = o.sumpot;
+        status[z] = *E.status;
+    }
+}
+
+static SmemPlan plan_for(const sgp_model *m, int allow_mats) {
+    return sgp_smem_plan(m->dev.mp.d, m->dev.mp.Dtot, allow_mats);
+}
+
+extern "C" int sgp_eval(const sgp_model *m, int Z, const double *d_tau, const double *d_q, int what, double *d_pot,
+                        double *d_grad, double *d_hess, double *d_sumpot, int *d_status, double *d_scratch,
+                        void *stream) {
+    if (!m || Z < 1 || !d_tau || !d_q || !d_status || !d_scratch) return SGP_EINVAL;
+    if ((what & SGP_EVAL_GRADIENT) && !d_grad) return SGP_EINVAL;
+    if ((what & SGP_EVAL_HESSIAN) && !d_hess) return SGP_EINVAL;
+    SmemPlan pl = plan_for(m, 0);
+    int rc = launch_prep(k_eval, pl.bytes);
+    if (rc) return rc;
+    k_eval<<<Z, SGP_NT, pl.bytes, S(stream)>>>(m->dev, pl, d_tau, d_q, what & 15, d_pot, d_grad, d_hess, d_sumpot,
+                                                 d_status, d_scratch, sgp_scratch_doubles(m));
+    return check_launch();
+}
+
+__global__ void __launch_bounds__(SGP_NT) k_trace(ModelDev M, SmemPlan pl, const double *tau, const double *q,
+                                                  const double *Win, double *tout, int *status, double *scratch,
+                                                  size_t spc) {
+    const int z = blockIdx.x;
+    const int d = M.mp.d;
+    ChainWS w;
+    EvalCtx E;
+    setup_ws(w, E, sgp_smem, pl, M, scratch + (size_t)z * spc);
+    for (int j = threadIdx.x; j < d; j += SGP_NT) w.q0[j] = q[(size_t)z * d + j];
+    const double *Wz = Win + (size_t)z * d * d;
+    for (int idx = threadIdx.x; idx < d * d; idx += SGP_NT) {
+        const int i = idx / d, k = idx - i * d;
+        w.W[idx] = 0.5 * (Wz[idx] + Wz[k * d + i]);
+    }
+    __syncthreads();
+    EvalOut o;
+    eval_state(E, w.q0, tau[z], 0, w.grad, w.H, o);
+    if (*E.status == 0) eval_trace(E, w.q0, tau[z], w.W, w.tv);
+    for (int j = threadIdx.x; j < d; j += SGP_NT) tout[(size_t)z * d + j] = w.tv[j];
+    if (threadIdx.x == 0) status[z] = *E.status;
+}
+
+extern "C" int sgp_trace(const sgp_model *m, int Z, const double *d_tau, const double *d_q, const double *d_w,
+                         double *d_t, int *d_status, double *d_scratch, void *stream) {
+    if (!m || Z < 1 || !d_tau || !d_q || !d_w || !d_t || !d_status || !d_scratch) return SGP_EINVAL;
+    SmemPlan pl = plan_for(m, 0);
+    int rc = launch_prep(k_trace, pl.bytes);
+    if (rc) return rc;
+    k_trace<<<Z, SGP_NT, pl.bytes, S(stream)>>>(m->dev, pl, d_tau, d_q, d_w, d_t, d_status, d_scratch,
+                                                  sgp_scratch_doubles(m));
+    return check_launch();
+}
+
+__global__ void k_potential_derivatives(int lik, int n, int J, const double *f, const double *y, double vfloor,
+                                        double *u, double *d1, double *d2, double *d3) {
+    double S[F_COUNT];
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const double f0 = f[(size_t)i * J], f1 = J == 2 ? f[(size_t)i * J + 1] : 0.0;
+        lik_sample(lik, vfloor, y[i], f0, f1, S, 1, 0);
+        u[i] = S[F_U];
+        if (J == 1) {
+            d1[i] = S[F_D1_0];
+            d2[i] = S[F_D2_00];
+            d3[i] = S[F_D3_000];
+        } else {
+            d1[2 * i] = S[F_D1_0];
+            d1[2 * i + 1] = S[F_D1_1];
+            double *h = d2 + 4 * (size_t)i;
+            h[0] = S[F_D2_00];
+            h[1] = h[2] = S[F_D2_01];
+            h[3] = S[F_D2_11];
+            double *t = d3 + 8 * (size_t)i;
+            t[0] = S[F_D3_000];
+            t[1] = t[2] = t[4] = S[F_D3_001];
+            t[3] = t[5] = t[6] = S[F_D3_011];
+            t[7] = S[F_D3_111];
+        }
+    }
+}
+
+extern "C" int sgp_potential_derivatives(int lik, int n, int J, const double *d_f, const double *d_y,
+                                         double variance_floor, double *d_u, double *d_d1, double *d_d2,
+                                         double *d_d3, void *stream) {
+    if (n < 1 || !d_f || !d_y || !d_u || !d_d1 || !d_d2 || !d_d3) return SGP_EINVAL;
+    if (!((lik == SGP_LIK_LOGISTIC && J == 1) || (lik == SGP_LIK_GAUSSIAN_MEANVAR && J == 2))) return SGP_EINVAL;
+    k_potential_derivatives<<<(n + 255) / 256, 256, 0, S(stream)>>>(lik, n, J, d_f, d_y, variance_floor, d_u, d_d1,
+                                                                    d_d2, d_d3);
+    return check_launch();
+}
+
+// ===========================================================================
+// eigensolvers
+
+__global__ void __launch_bounds__(SGP_NT) k_eigh_cold(int d, const double *Hin, double zeta, int cap, double *lam,
+                                                      double *psi, int *sweeps, double *tmp) {
+    __shared__ double red[64];
+    const int z = blockIdx.x;
+    const size_t dd = (size_t)d * d;
+    double *A = tmp + z * dd;
+    double *V = psi + z * dd;
+    const double *H = Hin + z * dd;
+    for (int idx = threadIdx.x; idx < d * d; idx += SGP_NT) {
+        const int i = idx / d, k = idx - i * d;
+        A[idx] = (i == k) ? H[idx] : 0.5 * (H[idx] + H[k * d + i]);
+        V[idx] = (i == k) ? 1.0 : 0.0;
+    }
+    __syncthreads();
+    const double hnorm = sqrt(frob2(A, d * d, red));
+    const double tol = zeta * hnorm;
+    const double skip = d ? tol / d : 0.0;
+    int sw = jacobi_cyclic(A, V, d, tol, skip, cap, red);
+    for (int j = threadIdx.x; j < d; j += SGP_NT) lam[(size_t)z * d + j] = A[j * d + j];
+    if (threadIdx.x == 0) sweeps[z] = sw;
+}
+
+extern "C" int sgp_eigh_cold(int Z, int d, const double *d_h, double zeta, int cap, double *d_lam, double *d_psi,
+                             int *d_sweeps, void *stream) {
+    if (Z < 1 || d < 1 || !d_h || !d_lam || !d_psi || !d_sweeps) return SGP_EINVAL;
+    double *tmp = nullptr;
+    CUDA_TRY(cudaMallocAsync(&tmp, sizeof(double) * Z * (size_t)d * d, S(stream)));
+    k_eigh_cold<<<Z, SGP_NT, 0, S(stream)>>>(d, d_h, zeta, cap, d_lam, d_psi, d_sweeps, tmp);
+    int rc = check_launch();
+    cudaFreeAsync(tmp, S(stream));
+    return rc;
+}
+
+__global__ void __launch_bounds__(SGP_NT) k_eigh_warm(int d, const double *Hin, const double *psi_prev,
+                                                      const int *since_prev, int gs, double zeta, int cap, int order,
+                                                      double *lam, double *psi, int *since_out, int *sweeps,
+                                                      double *tmp) {
+    __shared__ double red[64];
+    extern __shared__ __align__(16) char dyn[];
+    double *prm = reinterpret_cast<double *>(dyn);
+    const int z = blockIdx.x;
+    const size_t dd = (size_t)d * d;
+    double *A = tmp + 2 * z * dd, *X = A + dd;
+    double *V = psi + z * dd;
+    const double *H = Hin + z * dd;
+    for (int idx = threadIdx.x; idx < d * d; idx += SGP_NT) V[idx] = psi_prev[z * dd + idx];
+    __syncthreads();
+    int since = since_prev[z] + 1;
+    if (gs && since >= gs) {
+        mgs(V, d, red);
+        since = 0;
+    }
+    const double hnorm = sqrt(frob2(H, d * d, red));
+    mat_mul<2>(X, V, H, d);
+    mat_mul<0>(A, X, V, d);
+    mat_symmetrize(A, d);
+    const double tol = zeta * hnorm;
+    const double skip = d ? tol / d : 0.0;
+    int sw = order == SGP_ORDER_CYCLIC ? jacobi_cyclic(A, V, d, tol, skip, cap, red)
+                                       : jacobi_parallel(A, V, d, tol, skip, cap, red, prm);
+    for (int j = threadIdx.x; j < d; j += SGP_NT) lam[(size_t)z * d + j] = A[j * d + j];
+    if (threadIdx.x == 0) {
+        sweeps[z] = sw;
+        since_out[z] = since;
+    }
+}
+
+extern "C" int sgp_eigh_warm(int Z, int d, const double *d_h, const double *d_psi_prev, const int *d_since_prev,
+                             int gs_interval, double zeta, int cap, int order, double *d_lam, double *d_psi,
+                             int *d_since, int *d_sweeps, void *stream) {
+    if (Z < 1 || d < 1 || !d_h || !d_psi_prev || !d_since_prev || !d_lam || !d_psi || !d_since || !d_sweeps)
+        return SGP_EINVAL;
+    double *tmp = nullptr;
+    CUDA_TRY(cudaMallocAsync(&tmp, sizeof(double) * 2 * Z * (size_t)d * d, S(stream)));
+    size_t smem = (6 * (size_t)((d + 2) / 2) + 8) * sizeof(double);
+    int rc = launch_prep(k_eigh_warm, smem);
+    if (rc) return rc;
+    k_eigh_warm<<<Z, SGP_NT, smem, S(stream)>>>(d, d_h, d_psi_prev, d_since_prev, gs_interval, zeta, cap, order,
+                                                 d_lam, d_psi, d_since, d_sweeps, tmp);
+    rc = check_launch();
+    cudaFreeAsync(tmp, S(stream));
+    return rc;
+}
+
+__global__ void __launch_bounds__(SGP_NT) k_mgs(int d, double *psi) {
+    __shared__ double red[64];
+    mgs(psi + (size_t)blockIdx.x * d * d, d, red);
+}
+
+extern "C" int sgp_mgs(int Z, int d, double *d_psi, void *stream) {
+    if (Z < 1 || d < 1 || !d_psi) return SGP_EINVAL;
+    k_mgs<<<Z, SGP_NT, 0, S(stream)>>>(d, d_psi);
+    return check_launch();
+}
+
+// ===========================================================================
+// metric algebra
+
+__global__ void __launch_bounds__(SGP_NT) k_metric(int d, const double *psi, const double *lamv, double kappa,
+                                                   const double *pin, int op, int which, double *out, double *out2,
+                                                   double *tmp) {
+    __shared__ double red[64];
+    const int z = blockIdx.x;
+    const size_t dd = (size_t)d * d;
+    const double *P = psi + z * dd;
+    const double *lam = lamv + (size_t)z * d;
+    double *T = tmp + 3 * z * dd, *X = T + dd;
+    double *g = X + dd, *b = g + d, *t2 = b + d;
+    metric_g(lam, g, d, kappa, red);
+    __syncthreads();
+    const double *p = pin ? pin + (size_t)z * d : nullptr;
+    if (op == 0) {  // T matrix
+        t_matrix(out + z * dd, lam, g, d, kappa);
+    } else if (op == 1) {  // W1 / W2 / W2 - W1
+        const bool w1 = which & SGP_W_W1, w2 = which & SGP_W_W2;
+        if (w1) t_matrix(T, lam, g, d, kappa);
+        metric_w(out + z * dd, X, b, P, lam, g, T, p, d, w1, w2, w2 ? -1.0 : 1.0);
+    } else if (op == 2) {  // apply
+        metric_apply(out + (size_t)z * d, t2, P, g, p, d, which);
+    } else {  // scalars: quad, logdet
+        double ldv = 0.0;
+        for (int j = threadIdx.x; j < d; j += SGP_NT) ldv += log(g[j]);
+        ldv = block_sum(ldv, red);
+        double qv = p ? metric_quad(t2, P, g, p, d, red) : 0.0;
+        if (threadIdx.x == 0) {
+            if (out) out[z] = qv;
+            if (out2) out2[z] = ldv;
+        }
+    }
+}
+
+static int metric_launch(int Z, int d, const double *psi, const double *lam, double kappa, const double *p, int op,
+                         int which, double *out, double *out2, void *stream) {
+    double *tmp = nullptr;
+    CUDA_TRY(cudaMallocAsync(&tmp, sizeof(double) * Z * (3 * (size_t)d * d), S(stream)));
+    k_metric<<<Z, SGP_NT, 0, S(stream)>>>(d, psi, lam, kappa, p, op, which, out, out2, tmp);
+    int rc = check_launch();
+    cudaFreeAsync(tmp, S(stream));
+    return rc;
+}
+
+extern "C" int sgp_t_matrix(int Z, int d, const double *d_lam, double kappa, double *d_t, void *stream) {
+    if (Z < 1 || d < 1 || !d_lam || !d_t || !(kappa > 0.0)) return SGP_EINVAL;
+    return metric_launch(Z, d, d_lam /*unused psi*/, d_lam, kappa, nullptr, 0, 0, d_t, nullptr, stream);
+}
+
+extern "C" int sgp_metric_w(int Z, int d, const double *d_psi, const double *d_lam, double kappa, const double *d_p,
+                            int which, double *d_w, void *stream) {
+    if (Z < 1 || d < 1 || !d_psi || !d_lam || !d_w || which < 1 || which > 3) return SGP_EINVAL;
+    if ((which & SGP_W_W1) && !d_p) return SGP_EINVAL;
+    return metric_launch(Z, d, d_psi, d_lam, kappa, d_p, 1, which, d_w, nullptr, stream);
+}
+
+extern "C" int sgp_metric_apply(int Z, int d, const double *d_psi, const double *d_lam, double kappa,
+                                const double *d_v, int mode, double *d_out, void *stream) {
+    if (Z < 1 || d < 1 || !d_psi || !d_lam || !d_v || !d_out || mode < 0 || mode > 2) return SGP_EINVAL;
+    return metric_launch(Z, d, d_psi, d_lam, kappa, d_v, 2, mode, d_out, nullptr, stream);
+}
+
+extern "C" int sgp_metric_scalars(int Z, int d, const double *d_psi, const double *d_lam, double kappa,
+                                  const double *d_p, double *d_quad, double *d_logdet, void *stream) {
+    if (Z < 1 || d < 1 || !d_psi || !d_lam) return SGP_EINVAL;
+    return metric_launch(Z, d, d_psi, d_lam, kappa, d_p, 3, 0, d_quad, d_logdet, stream);
+}
+
+// ===========================================================================
+// integrator and chains
+
+__global__ void __launch_bounds__(SGP_NT) k_leapfrog(ModelDev M, SmemPlan pl, sgp_chain_config cfg,
+                                                     sgp_chain_state st, double *pio, sgp_leapfrog_diag dgo,
+                                                     size_t spc) {
+    const int z = blockIdx.x;
+    const int d = M.mp.d;
+    const size_t dd = (size_t)d * d;
+    ChainWS w;
+    EvalCtx E;
+    setup_ws(w, E, sgp_smem, pl, M, st.scratch + (size_t)z * spc);
+    const double tau = st.tau[z];
+    for (int j = threadIdx.x; j < d; j += SGP_NT) {
+        w.q0[j] = st.q[(size_t)z * d + j];
+        w.p[j] = pio[(size_t)z * d + j];
+    }
+    __syncthreads();
+    int f = 0;
+    int s = frame_resume(w, E, cfg, tau, st.psi + z * dd, st.lam + (size_t)z * d, st.since[z], f);
+    LFDiag dg;
+    dg.fp_p = dg.fp_q = dg.nsweep = dg.sweep_cnt = 0;
+    dg.sweep_sum = 0.0;
+    if (!s) {
+        if (cfg.metric == SGP_METRIC_EUCLIDEAN)
+            s = leapfrog_euclid(w, E, cfg, tau);
+        else
+            s = leapfrog_riemann(w, E, cfg, tau, f, dg);
+    }
+    if (!s) {
+        for (int j = threadIdx.x; j < d; j += SGP_NT) {
+            st.q[(size_t)z * d + j] = w.q0[j];
+            pio[(size_t)z * d + j] = w.p[j];
+        }
+        if (cfg.metric != SGP_METRIC_EUCLIDEAN) {
+            for (int idx = threadIdx.x; idx < d * d; idx += SGP_NT) st.psi[z * dd + idx] = w.P[f][idx];
+            for (int j = threadIdx.x; j < d; j += SGP_NT) st.lam[(size_t)z * d + j] = w.lam[f][j];
+        }
+    }
+    if (threadIdx.x == 0) {
+        st.status[z] = s;
+        if (!s && cfg.metric != SGP_METRIC_EUCLIDEAN) st.since[z] = w.si[f];
+        if (dgo.fp_p_iters) dgo.fp_p_iters[z] = dg.fp_p;
+        if (dgo.fp_q_iters) dgo.fp_q_iters[z] = dg.fp_q;
+        if (dgo.sweeps)
+            for (int k = 0; k < cfg.fp_max_iters; ++k)
+                dgo.sweeps[(size_t)z * cfg.fp_max_iters + k] = k < dg.nsweep && k < 32 ? dg.sweeps[k] : -1;
+    }
+}
+
+static int chain_plan(const sgp_model *m, SmemPlan &pl) {
+    pl = plan_for(m, 1);
+    return SGP_OK;
+}
+
+extern "C" int sgp_leapfrog(const sgp_model *m, const sgp_chain_config *cfg, const sgp_chain_state *st, double *d_p,
+                            sgp_leapfrog_diag *diag, void *stream) {
+    if (!m || !cfg || !st || !d_p || st->n_chains < 1) return SGP_EINVAL;
+    if (cfg->fp_max_iters < 1 || cfg->fp_max_iters > 32) return SGP_EINVAL;
+    SmemPlan pl;
+    chain_plan(m, pl);
+    int rc = launch_prep(k_leapfrog, pl.bytes);
+    if (rc) return rc;
+    sgp_leapfrog_diag dg = diag ? *diag : sgp_leapfrog_diag{nullptr, nullptr, nullptr};
+    k_leapfrog<<<st->n_chains, SGP_NT, pl.bytes, S(stream)>>>(m->dev, pl, *cfg, *st, d_p, dg,
+                                                                sgp_scratch_doubles(m));
+    return check_launch();
+}
+
+__global__ void __launch_bounds__(SGP_NT) k_chain_init(ModelDev M, SmemPlan pl, sgp_chain_config cfg,
+                                                       sgp_chain_state st, size_t spc) {
+    const int z = blockIdx.x;
+    const int d = M.mp.d;
+    const size_t dd = (size_t)d * d;
+    ChainWS w;
+    EvalCtx E;
+    setup_ws(w, E, sgp_smem, pl, M, st.scratch + (size_t)z * spc);
+    for (int j = threadIdx.x; j < d; j += SGP_NT) w.q0[j] = st.q[(size_t)z * d + j];
+    __syncthreads();
+    int f = 0;
+    int s = frame_build(w, E, cfg, st.tau[z], f);
+    if (!s && cfg.metric != SGP_METRIC_EUCLIDEAN) {
+        for (int idx = threadIdx.x; idx < d * d; idx += SGP_NT) st.psi[z * dd + idx] = w.P[0][idx];
+        for (int j = threadIdx.x; j < d; j += SGP_NT) st.lam[(size_t)z * d + j] = w.lam[0][j];
+    }
+    if (threadIdx.x == 0) {
+        st.status[z] = s ? SGP_STATUS_CHAIN_START : 0;
+        st.since[z] = 0;
+    }
+}
+
+extern "C" int sgp_chain_init(const sgp_model *m, const sgp_chain_config *cfg, const sgp_chain_state *st,
+                              void *stream) {
+    if (!m || !cfg || !st || st->n_chains < 1) return SGP_EINVAL;
+    SmemPlan pl;
+    chain_plan(m, pl);
+    int rc = launch_prep(k_chain_init, pl.bytes);
+    if (rc) return rc;
+    k_chain_init<<<st->n_chains, SGP_NT, pl.bytes, S(stream)>>>(m->dev, pl, *cfg, *st, sgp_scratch_doubles(m));
+    return check_launch();
+}
+
+// The MH move loop (sampler.py:355-411), C leapfrogs per move, all on device.
+__global__ void __launch_bounds__(SGP_NT) k_run_moves(ModelDev M, SmemPlan pl, sgp_chain_config cfg,
+                                                      sgp_chain_state st, int moves, int move_offset,
+                                                      const double *dz, const double *dlogu, sgp_move_records rec,
+                                                      size_t spc) {
+    const int z = blockIdx.x;
+    const int Z = st.n_chains;
+    const int d = M.mp.d;
+    const size_t dd = (size_t)d * d;
+    ChainWS w;
+    EvalCtx E;
+    setup_ws(w, E, sgp_smem, pl, M, st.scratch + (size_t)z * spc);
+    if (st.status[z] != 0) return;
+    const double tau = st.tau[z];
+    const bool euclid = cfg.metric == SGP_METRIC_EUCLIDEAN;
+    for (int j = threadIdx.x; j < d; j += SGP_NT) w.q0[j] = st.q[(size_t)z * d + j];
+    __syncthreads();
+    int f = 0;
+    int s = frame_resume(w, E, cfg, tau, st.psi + z * dd, st.lam + (size_t)z * d, st.since[z], f);
+    if (s) {
+        if (threadIdx.x == 0) st.status[z] = SGP_STATUS_CHAIN_START;
+        return;
+    }
+    int final_status = 0;
+    for (int mv = 0; mv < moves; ++mv) {
+        const unsigned long long t0 = globaltimer_ns();
+        const double *zz = dz + ((size_t)mv * Z + z) * d;
+        if (euclid) {
+            for (int j = threadIdx.x; j < d; j += SGP_NT) w.p[j] = zz[j];
+            __syncthreads();
+        } else {
+            for (int j = threadIdx.x; j < d; j += SGP_NT) w.pn[j] = zz[j];
+            __syncthreads();
+            metric_apply(w.p, w.tmp, w.P[f], w.g[f], w.pn, d, 2);
+        }
+        const double pot_before = w.sc[2];
+        const double h_before = pot_before + frame_kinetic(w, E, cfg, f);
+        for (int j = threadIdx.x; j < d; j += SGP_NT) w.qs[j] = w.q0[j];
+        __syncthreads();
+        LFDiag dg;
+        dg.fp_p = dg.fp_q = dg.nsweep = dg.sweep_cnt = 0;
+        dg.sweep_sum = 0.0;
+        int fr = f;
+        int ls = 0;
+        for (int l = 0; l < cfg.leapfrogs; ++l) {
+            ls = euclid ? leapfrog_euclid(w, E, cfg, tau) : leapfrog_riemann(w, E, cfg, tau, fr, dg);
+            if (ls) break;
+        }
+        bool div = ls != 0;
+        double h_after = NAN;
+        if (!div) {
+            h_after = w.sc[2] + frame_kinetic(w, E, cfg, fr);
+            if (!isfinite(h_after)) div = true;
+        }
+        if (div) h_after = NAN;
+        const bool accept = !div && (h_before - h_after) > dlogu[(size_t)mv * Z + z];
+        __syncthreads();
+        if (threadIdx.x == 0) *E.status = 0;
+        __syncthreads();
+        if (accept) {
+            f = fr;
+        } else {
+            if (div && mv + move_offset == 0) {
+                final_status = SGP_STATUS_FIRST_MOVE;
+            } else {
+                for (int j = threadIdx.x; j < d; j += SGP_NT) w.q0[j] = w.qs[j];
+                __syncthreads();
+                int rs = frame_build(w, E, cfg, tau, f);  // cold resync (sampler.py:392-397)
+                if (rs) final_status = rs;
+            }
+        }
+        const size_t ri = (size_t)mv * Z + z;
+        if (threadIdx.x == 0) {
+            rec.logpost[ri] = -w.sc[2];
+            rec.h_before[ri] = h_before;
+            rec.h_after[ri] = h_after;
+            rec.accept[ri] = accept;
+            rec.divergent[ri] = div;
+            rec.sweeps_mean[ri] = dg.sweep_cnt ? dg.sweep_sum / dg.sweep_cnt : 0.0;
+            rec.wall_ms[ri] = (double)(globaltimer_ns() - t0) * 1e-6;
+        }
+        if (rec.q)
+            for (int j = threadIdx.x; j < d; j += SGP_NT) rec.q[ri * d + j] = (final_status ? w.qs[j] : w.q0[j]);
+        if (final_status) break;
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < d; j += SGP_NT) st.q[(size_t)z * d + j] = w.q0[j];
+    if (!euclid && !final_status) {
+        for (int idx = threadIdx.x; idx < d * d; idx += SGP_NT) st.psi[z * dd + idx] = w.P[f][idx];
+        for (int j = threadIdx.x; j < d; j += SGP_NT) st.lam[(size_t)z * d + j] = w.lam[f][j];
+    }
+    if (threadIdx.x == 0) {
+        st.status[z] = final_status;
+        if (!euclid && !final_status) st.since[z] = w.si[f];
+    }
+}
+
+extern "C" int sgp_run_moves(const sgp_model *m, const sgp_chain_config *cfg, const sgp_chain_state *st, int moves,
+                             int move_offset, const double *d_z, const double *d_logu, sgp_move_records *rec,
+                             void *stream) {
+    if (!m || !cfg || !st || !rec || st->n_chains < 1 || moves < 0 || !d_z || !d_logu) return SGP_EINVAL;
+    if (cfg->fp_max_iters < 1 || cfg->leapfrogs < 1) return SGP_EINVAL;
+    if (!rec->logpost || !rec->h_before || !rec->h_after || !rec->accept || !rec->divergent || !rec->sweeps_mean ||
+        !rec->wall_ms)
+        return SGP_EINVAL;
+    if (moves == 0) return SGP_OK;
+    SmemPlan pl;
+    chain_plan(m, pl);
+    int rc = launch_prep(k_run_moves, pl.bytes);
+    if (rc) return rc;
+    k_run_moves<<<st->n_chains, SGP_NT, pl.bytes, S(stream)>>>(m->dev, pl, *cfg, *st, moves, move_offset, d_z,
+                                                                 d_logu, *rec, sgp_scratch_doubles(m));
+    return check_launch();
+}
+
+extern "C" int sgp_device_info(int *sm_count, int *cc_major, int *cc_minor) {
+    int dev = 0;
+    CUDA_TRY(cudaGetDevice(&dev));
+    cudaDeviceProp prop;
+    CUDA_TRY(cudaGetDeviceProperties(&prop, dev));
+    if (sm_count) *sm_count = prop.multiProcessorCount;
+    if (cc_major) *cc_major = prop.major;
+    if (cc_minor) *cc_minor = prop.minor;
+    return SGP_OK;
+}
+
+extern "C" const char *sgp_version(void) { return "sgp 0.1.0 sm_100a"; }

@@ -1,0 +1,496 @@
+// sgp_eval.cuh — posterior value, gradient, Hessian and the structured
+// third-order trace contraction for one chain per CTA
+// (posterior.py:336-542 in the reference).
+#pragma once
+#include "sgp_core.cuh"
+
+struct EvalCtx {
+    ModelDev M;
+    double *S;      // per-sample fields, F_COUNT x ld (global scratch)
+    double *stage;  // smem staging for a chunk of samples: Dtot*CH + 3*CH
+    int CH;         // samples per chunk
+    double *red;    // smem reduction scratch (>= 64 doubles)
+    int *status;    // smem status word
+};
+
+// Latent values and per-sample derivatives at q; returns sum_i U_i (i < N).
+// Sets DIVERGENCE for non-finite f (posterior.py:344-345).
+__device__ double eval_lik(EvalCtx &E, const double *q) {
+    const ModelParams &mp = E.M.mp;
+    const int ld = mp.ld, N = mp.N;
+    const double *phi = E.M.phi;
+    double su = 0.0;
+    bool bad = false;
+    for (int i = threadIdx.x; i < ld; i += SGP_NT) {
+        double f0 = 0.0, f1 = 0.0;
+        for (int a = 0; a < mp.D[0]; ++a) f0 += phi[a * ld + i] * q[a];
+        if (mp.J == 2)
+            for (int a = 0; a < mp.D[1]; ++a) f1 += phi[(mp.D[0] + a) * ld + i] * q[mp.fstart[1] + a];
+        if (i < N) {
+            if (!isfinite(f0) || !isfinite(f1)) bad = true;
+            E.S[F_F0 * ld + i] = f0;
+            E.S[F_F1 * ld + i] = f1;
+            lik_sample(mp.lik, mp.vfloor, E.M.y[i], f0, f1, E.S, ld, i);
+            su += E.S[F_U * ld + i];
+        } else {
+            // padding rows: zero weight everywhere
+            for (int k = 0; k < F_COUNT; ++k) E.S[k * ld + i] = 0.0;
+        }
+    }
+    if (bad) set_status(E.status, SGP_STATUS_DIVERGENCE);
+    return block_sum(su, E.red);
+}
+
+// ---------------------------------------------------------------------------
+// staging of a chunk of samples: stage[a*CH + ii] = phi[a, i0+ii]
+__device__ __forceinline__ void stage_chunk(EvalCtx &E, int i0) {
+    const ModelParams &mp = E.M.mp;
+    const int CH = E.CH, ld = mp.ld;
+    for (int idx = threadIdx.x; idx < mp.Dtot * CH; idx += SGP_NT) {
+        const int a = idx / CH, ii = idx - a * CH;
+        const int i = i0 + ii;
+        E.stage[idx] = (i < ld) ? E.M.phi[a * ld + i] : 0.0;
+    }
+}
+
+// Likelihood Hessian block sum_i tau d2_{j(a)j(b)}(i) phi_a(i) phi_b(i) for the
+// upper triangle of [0, Dtot)^2, written (and mirrored) into H (posterior.py:449-460).
+template <int J>
+__device__ void hess_lik(EvalCtx &E, double tau, double *H, int d) {
+    const ModelParams &mp = E.M.mp;
+    const int Dt = mp.Dtot, CH = E.CH, ld = mp.ld, D0 = mp.D[0];
+    const int nb = (Dt + 1) >> 1;
+    const int ntu = nb * (nb + 1) / 2;  // upper-triangle 2x2 tiles
+    double *wst = E.stage + Dt * CH;    // 3*CH weights
+    int R = 1;
+    if (ntu * 2 <= SGP_NT) R = min(4, SGP_NT / ntu);
+    const int per_pass = (R > 1) ? ntu : SGP_NT * 4;
+    for (int base = 0; base < ntu; base += per_pass) {
+        double acc[4][4];
+        int tiles[4];
+        int nmine = 0, rep = 0;
+        if (R > 1) {
+            if ((int)threadIdx.x < R * ntu) {
+                tiles[0] = threadIdx.x % ntu;
+                rep = threadIdx.x / ntu;
+                nmine = 1;
+            }
+        } else {
+            for (int s = 0; s < 4; ++s) {
+                int t = base + threadIdx.x + s * SGP_NT;
+                if (t < ntu) tiles[nmine++] = t;
+            }
+        }
+        int ti[4], tj[4];
+        for (int s = 0; s < nmine; ++s) {
+            // linear upper-triangle index -> (bi, bj), bi <= bj
+            int t = tiles[s], bi = 0;
+            while (t >= nb - bi) {
+                t -= nb - bi;
+                ++bi;
+            }
+            ti[s] = bi * 2;
+            tj[s] = (bi + t) * 2;
+            for (int e = 0; e < 4; ++e) acc[s][e] = 0.0;
+        }
+        for (int i0 = 0; i0 < ld; i0 += CH) {
+            __syncthreads();
+            stage_chunk(E, i0);
+            for (int ii = threadIdx.x; ii < CH; ii += SGP_NT) {
+                const int i = i0 + ii;
+                const bool ok = i < mp.N;
+                wst[ii] = ok ? tau * E.S[F_D2_00 * ld + i] : 0.0;
+                if (J == 2) {
+                    wst[CH + ii] = ok ? tau * E.S[F_D2_01 * ld + i] : 0.0;
+                    wst[2 * CH + ii] = ok ? tau * E.S[F_D2_11 * ld + i] : 0.0;
+                }
+            }
+            __syncthreads();
+            for (int s = 0; s < nmine; ++s) {
+                const int a0 = ti[s], b0 = tj[s];
+                const int a1 = min(a0 + 1, Dt - 1), b1 = min(b0 + 1, Dt - 1);
+                const double *pa0 = E.stage + a0 * CH, *pa1 = E.stage + a1 * CH;
+                const double *pb0 = E.stage + b0 * CH, *pb1 = E.stage + b1 * CH;
+                if (J == 1) {
+                    double c00 = acc[s][0], c01 = acc[s][1], c10 = acc[s][2], c11 = acc[s][3];
+                    for (int ii = rep; ii < CH; ii += R) {
+                        const double w = wst[ii];
+                        const double x0 = pa0[ii] * w, x1 = pa1[ii] * w;
+                        const double y0 = pb0[ii], y1 = pb1[ii];
+                        c00 += x0 * y0;
+                        c01 += x0 * y1;
+                        c10 += x1 * y0;
+                        c11 += x1 * y1;
+                    }
+                    acc[s][0] = c00;
+                    acc[s][1] = c01;
+                    acc[s][2] = c10;
+                    acc[s][3] = c11;
+                } else {
+                    const int ja0 = a0 >= D0, ja1 = a1 >= D0, jb0 = b0 >= D0, jb1 = b1 >= D0;
+                    const double *w00 = wst + (ja0 + jb0) * CH, *w01 = wst + (ja0 + jb1) * CH;
+                    const double *w10 = wst + (ja1 + jb0) * CH, *w11 = wst + (ja1 + jb1) * CH;
+                    double c00 = acc[s][0], c01 = acc[s][1], c10 = acc[s][2], c11 = acc[s][3];
+                    for (int ii = rep; ii < CH; ii += R) {
+                        const double x0 = pa0[ii], x1 = pa1[ii];
+                        const double y0 = pb0[ii], y1 = pb1[ii];
+                        c00 += x0 * w00[ii] * y0;
+                        c01 += x0 * w01[ii] * y1;
+                        c10 += x1 * w10[ii] * y0;
+                        c11 += x1 * w11[ii] * y1;
+                    }
+                    acc[s][0] = c00;
+                    acc[s][1] = c01;
+                    acc[s][2] = c10;
+                    acc[s][3] = c11;
+                }
+            }
+        }
+        // ordered reduction over replicas, then mirror
+        for (int r = 0; r < R; ++r) {
+            __syncthreads();
+            for (int s = 0; s < nmine; ++s) {
+                if (rep != r) continue;
+                const int a0 = ti[s], b0 = tj[s];
+                for (int e = 0; e < 4; ++e) {
+                    const int a = a0 + (e >> 1), b = b0 + (e & 1);
+                    if (a >= Dt || b >= Dt || a > b) continue;
+                    double v = acc[s][e];
+                    if (r > 0) v += H[a * d + b];
+                    H[a * d + b] = v;
+                    H[b * d + a] = v;
+                }
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// Per-sample quadratic forms s^(j1 j2)_i = phi_j1(x_i)^T W_blk phi_j2(x_i) and
+// their third-derivative contractions c^(j)_i (posterior.py:495-509).
+template <int J>
+__device__ void trace_lik_samples(EvalCtx &E, const double *W, int d) {
+    const ModelParams &mp = E.M.mp;
+    const int Dt = mp.Dtot, CH = E.CH, ld = mp.ld, D0 = mp.D[0];
+    const int G = SGP_NT / CH;
+    double *part = E.stage + Dt * CH;  // G * CH * 3
+    const int ii = threadIdx.x % CH, gi = threadIdx.x / CH;
+    for (int i0 = 0; i0 < ld; i0 += CH) {
+        __syncthreads();
+        stage_chunk(E, i0);
+        __syncthreads();
+        double s00 = 0.0, sx = 0.0, s11 = 0.0;
+        if (gi < G) {
+            for (int a = gi; a < Dt; a += G) {
+                const double *wr = W + a * d;
+                double y0 = 0.0, y1 = 0.0;
+                for (int b = 0; b < D0; ++b) y0 += wr[b] * E.stage[b * CH + ii];
+                if (J == 2)
+                    for (int b = D0; b < Dt; ++b) y1 += wr[b] * E.stage[b * CH + ii];
+                const double pa = E.stage[a * CH + ii];
+                if (a < D0) {
+                    s00 += pa * y0;
+                    sx += pa * y1;
+                } else {
+                    sx += pa * y0;
+                    s11 += pa * y1;
+                }
+            }
+            part[(gi * CH + ii) * 3 + 0] = s00;
+            part[(gi * CH + ii) * 3 + 1] = sx;
+            part[(gi * CH + ii) * 3 + 2] = s11;
+        }
+        __syncthreads();
+        if ((int)threadIdx.x < CH) {
+            const int i = i0 + threadIdx.x;
+            double a00 = 0.0, ax = 0.0, a11 = 0.0;
+            for (int g = 0; g < G; ++g) {
+                a00 += part[(g * CH + threadIdx.x) * 3 + 0];
+                ax += part[(g * CH + threadIdx.x) * 3 + 1];
+                a11 += part[(g * CH + threadIdx.x) * 3 + 2];
+            }
+            if (i < ld) {
+                if (i < mp.N) {
+                    if (J == 1) {
+                        E.S[F_C0 * ld + i] = E.S[F_D3_000 * ld + i] * a00;
+                    } else {
+                        const double t001 = E.S[F_D3_001 * ld + i], t011 = E.S[F_D3_011 * ld + i];
+                        const double t111 = E.S[F_D3_111 * ld + i];
+                        // d3[0,0,0] is structurally zero for the mean/variance likelihood
+                        E.S[F_C0 * ld + i] = t001 * ax + t011 * a11;
+                        E.S[F_C1 * ld + i] = t001 * a00 + t011 * ax + t111 * a11;
+                    }
+                } else {
+                    E.S[F_C0 * ld + i] = 0.0;
+                    E.S[F_C1 * ld + i] = 0.0;
+                }
+            }
+        }
+    }
+    __syncthreads();
+}
+
+// out[a] = tau * sum_i phi[a,i] * S[field(j(a)), i] for a < Dtot (warp per row).
+__device__ void project_back(EvalCtx &E, double tau, int field0, int field1, double *out) {
+    const ModelParams &mp = E.M.mp;
+    const int ld = mp.ld;
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    for (int a = w; a < mp.Dtot; a += SGP_NWARP) {
+        const int f = (a < mp.D[0]) ? field0 : field1;
+        const double *pr = E.M.phi + a * ld;
+        const double *sr = E.S + f * ld;
+        double s = 0.0;
+        for (int i = l; i < mp.N; i += 32) s += pr[i] * sr[i];
+        s = warp_sum(s);
+        if (l == 0) out[a] = tau * s;
+    }
+    __syncthreads();
+}
+
+// ---------------------------------------------------------------------------
+// Full evaluation at q.  what: SGP_EVAL_* bits.  Writes *pot (potential),
+// *sumpot (sum_i U_i), grad[d], H[d*d] as requested.  Status via E.status.
+
+// internal: per-sample fields in E.S already belong to q
+#define SGP_EVAL_REUSE 32
+
+struct EvalOut {
+    double pot, sumpot;
+};
+
+__device__ void eval_state(EvalCtx &E, const double *q, double tau, int what, double *grad, double *H, EvalOut &o) {
+    const ModelParams &mp = E.M.mp;
+    const int d = mp.d;
+    __syncthreads();
+    for (int a = threadIdx.x; a < d; a += SGP_NT)
+        if (!isfinite(q[a])) set_status(E.status, SGP_STATUS_DIVERGENCE);
+    __syncthreads();
+    o.pot = 0.0;
+    o.sumpot = 0.0;
+    if (*E.status) return;
+
+    if (mp.lik == SGP_LIK_QUADRATIC) {
+        // U = 0.5 r^T P r - tau c; grad = P r; H = P (tests/conftest.py:14-33)
+        const double *P = E.M.prec, *m = E.M.mean;
+        const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+        double part = 0.0;
+        for (int a = w; a < d; a += SGP_NWARP) {
+            double s = 0.0;
+            for (int b = l; b < d; b += 32) s += P[a * d + b] * (q[b] - m[b]);
+            s = warp_sum(s);
+            if (l == 0) {
+                if (what & SGP_EVAL_GRADIENT) grad[a] = s;
+                part += (q[a] - m[a]) * s;
+            }
+        }
+        double quadv = block_sum(part, E.red);
+        o.pot = 0.5 * quadv - tau * mp.loglik_const;
+        o.sumpot = -mp.loglik_const;
+        if (what & SGP_EVAL_HESSIAN) mat_copy(H, P, d * d);
+        return;
+    }
+
+    const bool need_lik = (tau != 0.0) || (what & SGP_EVAL_SUMPOT);
+    const bool reuse = (what & SGP_EVAL_REUSE) != 0;  // S already holds this point
+    double su = 0.0;
+    if (need_lik && !reuse) {
+        su = eval_lik(E, q);
+        __syncthreads();
+        if (*E.status) return;
+        o.sumpot = su;
+    }
+    const bool lik_on = tau != 0.0;
+
+    // likelihood gradient and Hessian parts
+    if (what & SGP_EVAL_GRADIENT) {
+        if (lik_on) {
+            project_back(E, tau, F_D1_0, F_D1_1, grad);
+            for (int a = mp.Dtot + threadIdx.x; a < d; a += SGP_NT) grad[a] = 0.0;
+        } else {
+            for (int a = threadIdx.x; a < d; a += SGP_NT) grad[a] = 0.0;
+        }
+        __syncthreads();
+    }
+    if (what & SGP_EVAL_HESSIAN) {
+        for (int idx = threadIdx.x; idx < d * d; idx += SGP_NT) H[idx] = 0.0;
+        __syncthreads();
+        if (lik_on) {
+            if (mp.J == 1)
+                hess_lik<1>(E, tau, H, d);
+            else
+                hess_lik<2>(E, tau, H, d);
+        }
+        __syncthreads();
+    }
+
+    // prior, intercept and hyperprior parts (thread per coordinate)
+    // partial sums: [0] potential, [1..3] hyper grad slots, [4..7] hyper Hessian (00, 01, 11, 22)
+    double ps[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int a = threadIdx.x; a < d; a += SGP_NT) {
+        const int kind = E.M.ckind[a];
+        const double qa = q[a];
+        if (kind == CK_GAUSS || kind == CK_LIN) {
+            CoefD c;
+            int st = coef_derivs(mp, kind, E.M.cw[a], q, c);
+            if (st) {
+                set_status(E.status, st);
+                continue;
+            }
+            const double a2 = qa * qa;
+            ps[0] += 0.5 * a2 * c.r - 0.5 * c.rho + 0.5 * SGP_LN_2PI;
+            if (what & SGP_EVAL_GRADIENT) grad[a] += qa * c.r;
+            if (what & SGP_EVAL_HESSIAN) H[a * d + a] += c.r;
+            for (int k = 0; k < c.h; ++k) {
+                const int slot = c.hs[k];
+                ps[1 + slot] += 0.5 * a2 * c.r1[k] - 0.5 * c.rho1[k];
+                if (what & SGP_EVAL_HESSIAN) {
+                    const int pk = mp.hpos[slot];
+                    H[a * d + pk] += qa * c.r1[k];
+                    H[pk * d + a] += qa * c.r1[k];
+                }
+            }
+            if (c.h == 2) {
+                ps[4] += 0.5 * a2 * c.r2[0] - 0.5 * c.rho2[0];
+                ps[5] += 0.5 * a2 * c.r2[1] - 0.5 * c.rho2[1];
+                ps[6] += 0.5 * a2 * c.r2[2] - 0.5 * c.rho2[2];
+            } else if (c.h == 1) {
+                ps[7] += 0.5 * a2 * c.r2[0] - 0.5 * c.rho2[0];
+            }
+        } else if (kind == CK_INTERCEPT) {
+            ps[0] += 0.5 * qa * qa / mp.sigma + 0.5 * log(2.0 * SGP_PI * mp.sigma);
+            if (what & SGP_EVAL_GRADIENT) grad[a] += qa / mp.sigma;
+            if (what & SGP_EVAL_HESSIAN) H[a * d + a] += 1.0 / mp.sigma;
+        }
+    }
+    block_sum_k<8>(ps, E.red);
+    __syncthreads();
+    if (*E.status) return;
+    // hyper coordinates: group sums then hyperprior terms (one thread)
+    if (threadIdx.x == 0) {
+        double pot = lik_on ? tau * su : 0.0;
+        pot += ps[0];
+        for (int slot = 0; slot < 3; ++slot) {
+            const int pos = mp.hpos[slot];
+            if (pos < 0) continue;
+            if (what & SGP_EVAL_GRADIENT) grad[pos] += ps[1 + slot];
+        }
+        if (what & SGP_EVAL_HESSIAN) {
+            const int pc = mp.hpos[0], psg = mp.hpos[1], pl = mp.hpos[2];
+            if (pc >= 0 && mp.n_gauss > 0) {
+                H[pc * d + pc] += ps[4];
+                H[pc * d + psg] += ps[5];
+                H[psg * d + pc] += ps[5];
+                H[psg * d + psg] += ps[6];
+            }
+            if (pl >= 0 && mp.n_lin > 0) H[pl * d + pl] += ps[7];
+        }
+        for (int slot = 0; slot < 3; ++slot) {
+            const int pos = mp.hpos[slot];
+            if (pos < 0) continue;
+            double u[4];
+            int st = hyperprior(mp, slot, q[pos], u);
+            if (st) {
+                set_status(E.status, st);
+                break;
+            }
+            pot += u[0];
+            if (what & SGP_EVAL_GRADIENT) grad[pos] += u[1];
+            if (what & SGP_EVAL_HESSIAN) H[pos * d + pos] += u[2];
+        }
+        E.red[40] = pot;
+    }
+    __syncthreads();
+    o.pot = E.red[40];
+    if (*E.status) return;
+    // finiteness checks (posterior.py:411, 437, 479)
+    bool bad = false;
+    if (what & SGP_EVAL_GRADIENT)
+        for (int a = threadIdx.x; a < d; a += SGP_NT) bad |= !isfinite(grad[a]);
+    if (what & SGP_EVAL_HESSIAN)
+        for (int idx = threadIdx.x; idx < d * d; idx += SGP_NT) bad |= !isfinite(H[idx]);
+    if ((what & SGP_EVAL_POTENTIAL) && threadIdx.x == 0 && !isfinite(o.pot)) bad = true;
+    if (bad) set_status(E.status, SGP_STATUS_DIVERGENCE);
+    __syncthreads();
+}
+
+// t = tr(W dH/dq_i) at the point whose per-sample derivatives are in E.S
+// (posterior.py:486-542).  W must be symmetric (callers symmetrise).
+__device__ void eval_trace(EvalCtx &E, const double *q, double tau, const double *W, double *t) {
+    const ModelParams &mp = E.M.mp;
+    const int d = mp.d;
+    __syncthreads();
+    if (mp.lik == SGP_LIK_QUADRATIC) {
+        for (int a = threadIdx.x; a < d; a += SGP_NT) t[a] = 0.0;
+        __syncthreads();
+        return;
+    }
+    if (tau != 0.0) {
+        if (mp.J == 1)
+            trace_lik_samples<1>(E, W, d);
+        else
+            trace_lik_samples<2>(E, W, d);
+        project_back(E, tau, F_C0, F_C1, t);
+        for (int a = mp.Dtot + threadIdx.x; a < d; a += SGP_NT) t[a] = 0.0;
+    } else {
+        for (int a = threadIdx.x; a < d; a += SGP_NT) t[a] = 0.0;
+    }
+    __syncthreads();
+    // prior terms; hyper targets accumulate into slots
+    double hs[3] = {0.0, 0.0, 0.0};
+    for (int a = threadIdx.x; a < d; a += SGP_NT) {
+        const int kind = E.M.ckind[a];
+        if (kind != CK_GAUSS && kind != CK_LIN) continue;
+        CoefD c;
+        int st = coef_derivs(mp, kind, E.M.cw[a], q, c);
+        if (st) {
+            set_status(E.status, st);
+            continue;
+        }
+        if (c.h == 0) continue;
+        const double qa = q[a], a2 = qa * qa;
+        double cols[2], hw[2][2];
+        for (int k = 0; k < c.h; ++k) {
+            const int pk = mp.hpos[c.hs[k]];
+            cols[k] = 0.5 * (W[a * d + pk] + W[pk * d + a]);
+            for (int l = 0; l < c.h; ++l) {
+                const int pl = mp.hpos[c.hs[l]];
+                hw[k][l] = 0.5 * (W[pk * d + pl] + W[pl * d + pk]);
+            }
+        }
+        double acc = 0.0;
+        for (int k = 0; k < c.h; ++k) {
+            acc += 2.0 * cols[k] * c.r1[k];
+            for (int l = 0; l < c.h; ++l) acc += hw[k][l] * qa * c.r2[k + l];
+        }
+        t[a] += acc;
+        const double waa = W[a * d + a];
+        for (int m = 0; m < c.h; ++m) {
+            double v = waa * c.r1[m];
+            for (int k = 0; k < c.h; ++k) {
+                v += 2.0 * cols[k] * (qa * c.r2[m + k]);
+                for (int l = 0; l < c.h; ++l) v += hw[k][l] * (0.5 * a2 * c.r3[m + k + l] - 0.5 * c.rho3[m + k + l]);
+            }
+            hs[c.hs[m]] += v;
+        }
+    }
+    block_sum_k<3>(hs, E.red);
+    if (threadIdx.x == 0) {
+        for (int slot = 0; slot < 3; ++slot) {
+            const int pos = mp.hpos[slot];
+            if (pos < 0) continue;
+            t[pos] += hs[slot];
+            double u[4];
+            int st = hyperprior(mp, slot, q[pos], u);
+            if (st) {
+                set_status(E.status, st);
+                break;
+            }
+            t[pos] += W[pos * d + pos] * u[3];
+        }
+    }
+    __syncthreads();
+    bool bad = false;
+    for (int a = threadIdx.x; a < d; a += SGP_NT) bad |= !isfinite(t[a]);
+    if (bad) set_status(E.status, SGP_STATUS_DIVERGENCE);
+    __syncthreads();
+}

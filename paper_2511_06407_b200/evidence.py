@@ -1,0 +1,273 @@
+"""Thermodynamic-integration model evidence on one or many B200s.
+
+Drop-in for ``softabs_gp.evidence.thermo_integrate`` (/root/reference/pkg/src/
+softabs_gp/evidence.py:184-274) with the same seeding, warm-up gating, ladder
+walk and aggregation, so the estimate for a given seed is the reference's.
+What changes is how chains execute:
+
+* all chains of a rank advance together: per rung one cold-start launch and
+  one on-device move-loop launch for the whole batch (one CTA per chain);
+* chains are sharded across ranks (chain z on rank z mod W) when
+  ``torch.distributed`` is initialised; rungs are never split;
+* the only collective is one all-gather of the per-chain rung values
+  (NCCL on GPU ranks, gloo in CPU tests), after the ladder.
+
+Chain results depend only on (seed, z), so estimates are bitwise identical
+for any world size.
+"""
+
+from __future__ import annotations
+
+import dataclasses
+import json
+import math
+
+import numpy as np
+
+from .metric import JacobiError
+from .posterior import PosteriorTarget
+from .sampler import ChainConfig, ChainError, run_chain, run_chains, wilcoxon_split_half
+
+
+@dataclasses.dataclass(frozen=True)
+class TemperLadder:
+    """Temperature schedule and per-rung effort (evidence.py:34-66)."""
+
+    taus: np.ndarray
+    moves_per_rung: int = 50
+    leapfrogs: int = 100
+    chains: int = 10
+
+    def __post_init__(self):
+        taus = np.asarray(self.taus, dtype=float)
+        object.__setattr__(self, "taus", taus)
+        if taus.ndim != 1 or taus.shape[0] < 2:
+            raise ValueError("ladder needs at least two rungs")
+        if taus[0] != 1.0 or taus[-1] != 0.0:
+            raise ValueError("ladder must start at tau = 1 and end at tau = 0")
+        if not np.all(np.diff(taus) < 0.0):
+            raise ValueError("ladder temperatures must strictly decrease")
+        if self.moves_per_rung < 1 or self.leapfrogs < 1 or self.chains < 1:
+            raise ValueError("moves_per_rung, leapfrogs and chains must be positive")
+
+    @property
+    def size(self):
+        return self.taus.shape[0]
+
+    def thin(self, factor):
+        if factor < 1:
+            raise ValueError("thinning factor must be at least 1")
+        idx = list(range(0, self.size, factor))
+        if idx[-1] != self.size - 1:
+            idx.append(self.size - 1)
+        return dataclasses.replace(self, taus=self.taus[idx])
+
+
+def default_ladder(moves_per_rung=50, leapfrogs=100, chains=10):
+    """The 101-rung schedule (evidence.py:69-80)."""
+    taus = np.empty(101)
+    taus[:41] = 1.0 - 0.02 * np.arange(41)
+    taus[41:71] = 0.2 - 0.005 * np.arange(1, 31)
+    taus[71:91] = 0.05 - 0.002 * np.arange(1, 21)
+    taus[91:] = 0.01 - 0.001 * np.arange(1, 11)
+    taus[0], taus[-1] = 1.0, 0.0
+    return TemperLadder(taus=taus, moves_per_rung=moves_per_rung, leapfrogs=leapfrogs, chains=chains)
+
+
+def trapezoid(values, taus):
+    return float(np.sum(0.5 * (values[1:] + values[:-1]) * -np.diff(taus)))
+
+
+def ti_variance(rung_variances, ladder):
+    taus = ladder.taus if hasattr(ladder, "taus") else np.asarray(ladder, dtype=float)
+    v = np.asarray(rung_variances, dtype=float)
+    if v.shape != taus.shape:
+        raise ValueError("need one variance per rung")
+    dt = np.diff(taus)
+    total = v[0] * dt[0] ** 2 + v[-1] * dt[-1] ** 2
+    if v.shape[0] > 2:
+        total += float(np.sum(v[1:-1] * (dt[:-1] ** 2 + dt[1:] ** 2)))
+    return 0.25 * float(total)
+
+
+@dataclasses.dataclass
+class EvidenceEstimate:
+    bme_mean: float
+    bme_stderr: float
+    per_chain: list
+    rung_means: list
+    ladder: TemperLadder
+    warnings: list
+    rung_values: np.ndarray | None = None
+
+    def to_json(self):
+        return json.dumps({"bme_mean": self.bme_mean, "bme_stderr": self.bme_stderr,
+                           "per_chain": self.per_chain, "ladder": [float(t) for t in self.ladder.taus],
+                           "rung_means": self.rung_means, "warnings": self.warnings}, indent=2)
+
+
+def warm_up(target, config, seqs, segment_moves, pvalue, warnings, initial, runner=run_chain):
+    """Segments at tau = 1 until the split-half trend test passes (evidence.py:125-139)."""
+    q = target.initial_point() if initial is None else np.asarray(initial, dtype=float)
+    for seq in seqs:
+        cfg = dataclasses.replace(config, moves=segment_moves, burnin=0, record_q=False, seed=seq)
+        res = runner(target, cfg, initial=q)
+        q = res.q_final
+        if segment_moves >= 10:
+            _, p = wilcoxon_split_half(res.logpost)
+            if p > pvalue:
+                return q
+    warnings.append(f"warm-up trend still visible after {len(seqs)} segments")
+    return q
+
+
+def device_ladder_runner(target, chain_seqs, q_warm, ladder, config, rung_average, spread_moves):
+    """Walk every chain in ``chain_seqs`` down the ladder as one device batch.
+
+    Returns (values (n, S) with NaN rows for chains that raised ChainError,
+    list of error strings or None) -- the per-chain outcome of evidence.py:166-181.
+    """
+    n = len(chain_seqs)
+    S = ladder.size
+    values = np.full((n, S), np.nan)
+    errors = [None] * n
+    subs = [seq.spawn(S + 1) for seq in chain_seqs]
+    q = np.tile(np.asarray(q_warm, dtype=float), (n, 1))
+    alive = list(range(n))
+
+    def step(tgt, cfg, seeds_of):
+        nonlocal alive
+        results = run_chains(tgt, cfg, [seeds_of(k) for k in alive], q[alive])
+        keep = []
+        for k, res in zip(alive, results):
+            if isinstance(res, ChainError):
+                errors[k] = str(res)
+                continue
+            if isinstance(res, Exception):
+                raise res
+            q[k] = res.q_final
+            keep.append((k, res))
+        alive = [k for k, _ in keep]
+        return keep
+
+    if spread_moves > 0 and alive:
+        step(target, dataclasses.replace(config, moves=spread_moves, burnin=0, record_q=False),
+             lambda k: subs[k][0])
+    for s, tau in enumerate(ladder.taus):
+        if not alive:
+            break
+        cfg = dataclasses.replace(config, moves=ladder.moves_per_rung, leapfrogs=ladder.leapfrogs,
+                                  burnin=0, record_q=rung_average)
+        keep = step(target.at_temperature(float(tau)), cfg, lambda k: subs[k][s + 1])
+        if not keep:
+            continue
+        if rung_average:
+            for k, res in keep:
+                values[k, s] = float(np.mean(target.log_likelihoods(res.sample_matrix())))
+        else:
+            idx = [k for k, _ in keep]
+            values[idx, s] = target.log_likelihoods(q[idx])
+    for k in range(n):
+        if errors[k] is not None:
+            values[k] = np.nan
+    return values, errors
+
+
+def _dist_info():
+    try:
+        import torch.distributed as dist
+
+        if dist.is_available() and dist.is_initialized():
+            return dist, dist.get_rank(), dist.get_world_size()
+    except Exception:
+        pass
+    return None, 0, 1
+
+
+def gather_chain_values(local_ids, local_values, n_chains, n_rungs):
+    """All-gather per-chain rung values to every rank; returns (Z, S) in chain order.
+
+    One ``all_gather_into_tensor`` of a padded [ceil(Z/W), S+1] block per rank
+    (column 0 = chain id + 1, 0 marks padding).  NCCL for GPU ranks, gloo on CPU.
+    """
+    import torch
+
+    dist, rank, world = _dist_info()
+    full = np.full((n_chains, n_rungs), np.nan)
+    if dist is None or world == 1:
+        for k, z in enumerate(local_ids):
+            full[z] = local_values[k]
+        return full
+    per = (n_chains + world - 1) // world
+    block = np.zeros((per, n_rungs + 1))
+    for k, z in enumerate(local_ids):
+        block[k, 0] = z + 1
+        block[k, 1:] = local_values[k]
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    src = torch.as_tensor(block, dtype=torch.float64, device=dev)
+    out = torch.empty((world * per, n_rungs + 1), dtype=torch.float64, device=dev)
+    dist.all_gather_into_tensor(out, src)
+    allb = out.cpu().numpy()
+    for row in allb:
+        if row[0] > 0:
+            full[int(row[0]) - 1] = row[1:]
+    return full
+
+
+def thermo_integrate(model, data, ladder, config, *, rung_average=False, warmup_segment_moves=50,
+                     warmup_max_segments=8, warmup_pvalue=0.05, spread_moves=10, initial=None,
+                     threads=1, progress=None, target=None, ladder_runner=None,
+                     warmup_runner=None):
+    """Estimate ln P(X) by thermodynamic integration (evidence.py:184-274).
+
+    ``threads`` is accepted for API compatibility; chains run as one device
+    batch per rank instead of a process pool.  ``ladder_runner`` /
+    ``warmup_runner`` substitute the chain executors (tests inject the CPU
+    oracle to exercise the multi-rank logic without a GPU).
+    """
+    if not isinstance(config, ChainConfig) and ladder_runner is None:
+        raise TypeError("config must be a ChainConfig")
+    seed_root = config.seed if isinstance(config.seed, np.random.SeedSequence) \
+        else np.random.SeedSequence(config.seed)
+    n_chains = ladder.chains
+    seqs = seed_root.spawn(warmup_max_segments + n_chains)
+    if target is None:
+        target = PosteriorTarget(model, data)
+    warnings: list = []
+    q_warm = warm_up(target, config, seqs[:warmup_max_segments], warmup_segment_moves, warmup_pvalue,
+                     warnings, initial, runner=warmup_runner or run_chain)
+    _, rank, world = _dist_info()
+    mine = [z for z in range(n_chains) if z % world == rank]
+    runner = ladder_runner or device_ladder_runner
+    vals, errs = runner(target, [seqs[warmup_max_segments + z] for z in mine], q_warm, ladder, config,
+                        rung_average, spread_moves)
+    # failure flags travel as an all-NaN row (the reference maps them to NaN too)
+    rung_values = gather_chain_values(mine, vals, n_chains, ladder.size)
+    if progress is not None:
+        progress(f"evidence: {n_chains} chains finished on {world} rank(s)")
+    per_chain = []
+    for z in range(n_chains):
+        row = rung_values[z]
+        if np.all(np.isnan(row)):
+            warnings.append(f"chain {z} flagged: chain failed")
+            per_chain.append(math.nan)
+            continue
+        per_chain.append(trapezoid(row, ladder.taus))
+    finite = [v for v in per_chain if math.isfinite(v)]
+    if not finite:
+        raise ChainError("all evidence chains failed")
+    bme_mean = float(np.mean(finite))
+    if len(finite) > 1:
+        bme_stderr = float(np.std(finite, ddof=1) / math.sqrt(len(finite)))
+    else:
+        bme_stderr = math.nan
+        warnings.append("single surviving chain; standard error undefined")
+    with np.errstate(invalid="ignore"):
+        rung_means = np.nanmean(rung_values, axis=0)
+    return EvidenceEstimate(bme_mean=bme_mean, bme_stderr=bme_stderr, per_chain=per_chain,
+                            rung_means=[float(v) for v in rung_means], ladder=ladder,
+                            warnings=warnings, rung_values=rung_values)
+
+
+__all__ = ["TemperLadder", "default_ladder", "ti_variance", "EvidenceEstimate", "thermo_integrate",
+           "gather_chain_values", "device_ladder_runner", "warm_up", "JacobiError"]
