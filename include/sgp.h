@@ -227,6 +227,11 @@ int sgp_run_moves(const sgp_model *model, const sgp_chain_config *cfg,
                   const double *d_z, const double *d_logu, sgp_move_records *rec,
                   void *stream);
 
+/* Diagnostics: cycles spent by chain 0 in each leapfrog phase (clock64), 16
+ * slots: 0 W formation, 1 trace contraction, 2 state + Hessian, 3 MGS,
+ * 4 Psi^T H Psi, 5 warm Jacobi, 8 cold Jacobi, 9 whole leapfrog. */
+int sgp_debug_phase_cycles(unsigned long long *h_out16, int reset);
+
 /* Device properties the host reports (SM count, name) and library version. */
 int sgp_device_info(int *sm_count, int *cc_major, int *cc_minor);
 const char *sgp_version(void);

@@ -248,7 +248,7 @@ extern "C" int sgp_model_phi(const sgp_model *m, int j, double *d_out, void *str
 // ===========================================================================
 // posterior evaluation
 
-__global__ void __launch_bounds__(SGP_NT) k_eval(ModelDev M, SmemPlan pl, const double *tau, const double *q, int what,
+__global__ void __launch_bounds__(SGP_MAX_NT) k_eval(ModelDev M, SmemPlan pl, const double *tau, const double *q, int what,
                                                  double *pot, double *grad, double *hess, double *sumpot, int *status,
                                                  double *scratch, size_t spc) {
     const int z = blockIdx.x;
@@ -271,7 +271,31 @@ __global__ void __launch_bounds__(SGP_NT) k_eval(ModelDev M, SmemPlan pl, const 
 }
 
 static SmemPlan plan_for(const sgp_model *m, int allow_mats) {
-    return sgp_smem_plan(m->dev.mp.d, m->dev.mp.Dtot, allow_mats);
+    return sgp_smem_plan(m->dev.mp.d, m->dev.mp.Dtot, SGP_MAX_NT, allow_mats ? 200 * 1024 : 0);
+}
+
+// Launch shape of the fused chain kernel: threads per CTA and the number of
+// CTAs (chains) meant to share an SM.  Small models run 64-thread CTAs, eight
+// per SM, with their d x d matrices in L2-resident scratch: the reference-order
+// Jacobi is a serial ~500-cycle-per-rotation chain, so throughput comes from
+// overlapping many chains per SM.  SGP_CHAIN_THREADS=64|128|256 overrides.
+struct ChainLaunch {
+    int nt, per_sm;
+    SmemPlan pl;
+};
+static ChainLaunch chain_launch(const sgp_model *m) {
+    int nt = m->dev.mp.d <= 64 ? 32 : 256;
+    const char *env = getenv("SGP_CHAIN_THREADS");
+    if (env) {
+        int v = atoi(env);
+        if (v == 32 || v == 64 || v == 128 || v == 256) nt = v;
+    }
+    ChainLaunch L;
+    L.nt = nt;
+    L.per_sm = nt == 32 ? 16 : (nt == 64 ? 8 : (nt == 128 ? 4 : 2));
+    const size_t budget = (227 * 1024) / L.per_sm - 1024;
+    L.pl = sgp_smem_plan(m->dev.mp.d, m->dev.mp.Dtot, nt, budget);
+    return L;
 }
 
 extern "C" int sgp_eval(const sgp_model *m, int Z, const double *d_tau, const double *d_q, int what, double *d_pot,
@@ -283,12 +307,12 @@ extern "C" int sgp_eval(const sgp_model *m, int Z, const double *d_tau, const do
     SmemPlan pl = plan_for(m, 0);
     int rc = launch_prep(k_eval, pl.bytes);
     if (rc) return rc;
-    k_eval<<<Z, SGP_NT, pl.bytes, S(stream)>>>(m->dev, pl, d_tau, d_q, what & 15, d_pot, d_grad, d_hess, d_sumpot,
+    k_eval<<<Z, SGP_MAX_NT, pl.bytes, S(stream)>>>(m->dev, pl, d_tau, d_q, what & 15, d_pot, d_grad, d_hess, d_sumpot,
                                                  d_status, d_scratch, sgp_scratch_doubles(m));
     return check_launch();
 }
 
-__global__ void __launch_bounds__(SGP_NT) k_trace(ModelDev M, SmemPlan pl, const double *tau, const double *q,
+__global__ void __launch_bounds__(SGP_MAX_NT) k_trace(ModelDev M, SmemPlan pl, const double *tau, const double *q,
                                                   const double *Win, double *tout, int *status, double *scratch,
                                                   size_t spc) {
     const int z = blockIdx.x;
@@ -316,7 +340,7 @@ extern "C" int sgp_trace(const sgp_model *m, int Z, const double *d_tau, const d
     SmemPlan pl = plan_for(m, 0);
     int rc = launch_prep(k_trace, pl.bytes);
     if (rc) return rc;
-    k_trace<<<Z, SGP_NT, pl.bytes, S(stream)>>>(m->dev, pl, d_tau, d_q, d_w, d_t, d_status, d_scratch,
+    k_trace<<<Z, SGP_MAX_NT, pl.bytes, S(stream)>>>(m->dev, pl, d_tau, d_q, d_w, d_t, d_status, d_scratch,
                                                   sgp_scratch_doubles(m));
     return check_launch();
 }
@@ -361,7 +385,7 @@ extern "C" int sgp_potential_derivatives(int lik, int n, int J, const double *d_
 // ===========================================================================
 // eigensolvers
 
-__global__ void __launch_bounds__(SGP_NT) k_eigh_cold(int d, const double *Hin, double zeta, int cap, double *lam,
+__global__ void __launch_bounds__(SGP_MAX_NT) k_eigh_cold(int d, const double *Hin, double zeta, int cap, double *lam,
                                                       double *psi, int *sweeps, double *tmp) {
     __shared__ double red[64];
     const int z = blockIdx.x;
@@ -388,13 +412,13 @@ extern "C" int sgp_eigh_cold(int Z, int d, const double *d_h, double zeta, int c
     if (Z < 1 || d < 1 || !d_h || !d_lam || !d_psi || !d_sweeps) return SGP_EINVAL;
     double *tmp = nullptr;
     CUDA_TRY(cudaMallocAsync(&tmp, sizeof(double) * Z * (size_t)d * d, S(stream)));
-    k_eigh_cold<<<Z, SGP_NT, 0, S(stream)>>>(d, d_h, zeta, cap, d_lam, d_psi, d_sweeps, tmp);
+    k_eigh_cold<<<Z, SGP_MAX_NT, 0, S(stream)>>>(d, d_h, zeta, cap, d_lam, d_psi, d_sweeps, tmp);
     int rc = check_launch();
     cudaFreeAsync(tmp, S(stream));
     return rc;
 }
 
-__global__ void __launch_bounds__(SGP_NT) k_eigh_warm(int d, const double *Hin, const double *psi_prev,
+__global__ void __launch_bounds__(SGP_MAX_NT) k_eigh_warm(int d, const double *Hin, const double *psi_prev,
                                                       const int *since_prev, int gs, double zeta, int cap, int order,
                                                       double *lam, double *psi, int *since_out, int *sweeps,
                                                       double *tmp) {
@@ -438,28 +462,28 @@ extern "C" int sgp_eigh_warm(int Z, int d, const double *d_h, const double *d_ps
     size_t smem = (6 * (size_t)((d + 2) / 2) + 8) * sizeof(double);
     int rc = launch_prep(k_eigh_warm, smem);
     if (rc) return rc;
-    k_eigh_warm<<<Z, SGP_NT, smem, S(stream)>>>(d, d_h, d_psi_prev, d_since_prev, gs_interval, zeta, cap, order,
+    k_eigh_warm<<<Z, SGP_MAX_NT, smem, S(stream)>>>(d, d_h, d_psi_prev, d_since_prev, gs_interval, zeta, cap, order,
                                                  d_lam, d_psi, d_since, d_sweeps, tmp);
     rc = check_launch();
     cudaFreeAsync(tmp, S(stream));
     return rc;
 }
 
-__global__ void __launch_bounds__(SGP_NT) k_mgs(int d, double *psi) {
+__global__ void __launch_bounds__(SGP_MAX_NT) k_mgs(int d, double *psi) {
     __shared__ double red[64];
     mgs(psi + (size_t)blockIdx.x * d * d, d, red);
 }
 
 extern "C" int sgp_mgs(int Z, int d, double *d_psi, void *stream) {
     if (Z < 1 || d < 1 || !d_psi) return SGP_EINVAL;
-    k_mgs<<<Z, SGP_NT, 0, S(stream)>>>(d, d_psi);
+    k_mgs<<<Z, SGP_MAX_NT, 0, S(stream)>>>(d, d_psi);
     return check_launch();
 }
 
 // ===========================================================================
 // metric algebra
 
-__global__ void __launch_bounds__(SGP_NT) k_metric(int d, const double *psi, const double *lamv, double kappa,
+__global__ void __launch_bounds__(SGP_MAX_NT) k_metric(int d, const double *psi, const double *lamv, double kappa,
                                                    const double *pin, int op, int which, double *out, double *out2,
                                                    double *tmp) {
     __shared__ double red[64];
@@ -496,7 +520,7 @@ static int metric_launch(int Z, int d, const double *psi, const double *lam, dou
                          int which, double *out, double *out2, void *stream) {
     double *tmp = nullptr;
     CUDA_TRY(cudaMallocAsync(&tmp, sizeof(double) * Z * (3 * (size_t)d * d), S(stream)));
-    k_metric<<<Z, SGP_NT, 0, S(stream)>>>(d, psi, lam, kappa, p, op, which, out, out2, tmp);
+    k_metric<<<Z, SGP_MAX_NT, 0, S(stream)>>>(d, psi, lam, kappa, p, op, which, out, out2, tmp);
     int rc = check_launch();
     cudaFreeAsync(tmp, S(stream));
     return rc;
@@ -529,7 +553,7 @@ extern "C" int sgp_metric_scalars(int Z, int d, const double *d_psi, const doubl
 // ===========================================================================
 // integrator and chains
 
-__global__ void __launch_bounds__(SGP_NT) k_leapfrog(ModelDev M, SmemPlan pl, sgp_chain_config cfg,
+__global__ void __launch_bounds__(SGP_MAX_NT) k_leapfrog(ModelDev M, SmemPlan pl, sgp_chain_config cfg,
                                                      sgp_chain_state st, double *pio, sgp_leapfrog_diag dgo,
                                                      size_t spc) {
     const int z = blockIdx.x;
@@ -549,6 +573,8 @@ __global__ void __launch_bounds__(SGP_NT) k_leapfrog(ModelDev M, SmemPlan pl, sg
     LFDiag dg;
     dg.fp_p = dg.fp_q = dg.nsweep = dg.sweep_cnt = 0;
     dg.sweep_sum = 0.0;
+    __shared__ int sweep_log[32];
+    dg.sweeps = sweep_log;
     if (!s) {
         if (cfg.metric == SGP_METRIC_EUCLIDEAN)
             s = leapfrog_euclid(w, E, cfg, tau);
@@ -590,12 +616,12 @@ extern "C" int sgp_leapfrog(const sgp_model *m, const sgp_chain_config *cfg, con
     int rc = launch_prep(k_leapfrog, pl.bytes);
     if (rc) return rc;
     sgp_leapfrog_diag dg = diag ? *diag : sgp_leapfrog_diag{nullptr, nullptr, nullptr};
-    k_leapfrog<<<st->n_chains, SGP_NT, pl.bytes, S(stream)>>>(m->dev, pl, *cfg, *st, d_p, dg,
+    k_leapfrog<<<st->n_chains, SGP_MAX_NT, pl.bytes, S(stream)>>>(m->dev, pl, *cfg, *st, d_p, dg,
                                                                 sgp_scratch_doubles(m));
     return check_launch();
 }
 
-__global__ void __launch_bounds__(SGP_NT) k_chain_init(ModelDev M, SmemPlan pl, sgp_chain_config cfg,
+__global__ void __launch_bounds__(SGP_MAX_NT) k_chain_init(ModelDev M, SmemPlan pl, sgp_chain_config cfg,
                                                        sgp_chain_state st, size_t spc) {
     const int z = blockIdx.x;
     const int d = M.mp.d;
@@ -624,12 +650,13 @@ extern "C" int sgp_chain_init(const sgp_model *m, const sgp_chain_config *cfg, c
     chain_plan(m, pl);
     int rc = launch_prep(k_chain_init, pl.bytes);
     if (rc) return rc;
-    k_chain_init<<<st->n_chains, SGP_NT, pl.bytes, S(stream)>>>(m->dev, pl, *cfg, *st, sgp_scratch_doubles(m));
+    k_chain_init<<<st->n_chains, SGP_MAX_NT, pl.bytes, S(stream)>>>(m->dev, pl, *cfg, *st, sgp_scratch_doubles(m));
     return check_launch();
 }
 
 // The MH move loop (sampler.py:355-411), C leapfrogs per move, all on device.
-__global__ void __launch_bounds__(SGP_NT) k_run_moves(ModelDev M, SmemPlan pl, sgp_chain_config cfg,
+template <int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB) k_run_moves(ModelDev M, SmemPlan pl, sgp_chain_config cfg,
                                                       sgp_chain_state st, int moves, int move_offset,
                                                       const double *dz, const double *dlogu, sgp_move_records rec,
                                                       size_t spc) {
@@ -670,6 +697,7 @@ __global__ void __launch_bounds__(SGP_NT) k_run_moves(ModelDev M, SmemPlan pl, s
         LFDiag dg;
         dg.fp_p = dg.fp_q = dg.nsweep = dg.sweep_cnt = 0;
         dg.sweep_sum = 0.0;
+        dg.sweeps = nullptr;
         int fr = f;
         int ls = 0;
         for (int l = 0; l < cfg.leapfrogs; ++l) {
@@ -734,12 +762,24 @@ extern "C" int sgp_run_moves(const sgp_model *m, const sgp_chain_config *cfg, co
         !rec->wall_ms)
         return SGP_EINVAL;
     if (moves == 0) return SGP_OK;
-    SmemPlan pl;
-    chain_plan(m, pl);
-    int rc = launch_prep(k_run_moves, pl.bytes);
-    if (rc) return rc;
-    k_run_moves<<<st->n_chains, SGP_NT, pl.bytes, S(stream)>>>(m->dev, pl, *cfg, *st, moves, move_offset, d_z,
-                                                                 d_logu, *rec, sgp_scratch_doubles(m));
+    const ChainLaunch L = chain_launch(m);
+    const size_t spc = sgp_scratch_doubles(m);
+    int rc;
+#define SGP_LAUNCH_MOVES(NT_, MB_)                                                                        \
+    rc = launch_prep(k_run_moves<NT_, MB_>, L.pl.bytes);                                                 \
+    if (rc) return rc;                                                                                    \
+    k_run_moves<NT_, MB_><<<st->n_chains, NT_, L.pl.bytes, S(stream)>>>(m->dev, L.pl, *cfg, *st, moves,    \
+                                                                        move_offset, d_z, d_logu, *rec, spc)
+    if (L.nt == 32) {
+        SGP_LAUNCH_MOVES(32, 16);
+    } else if (L.nt == 64) {
+        SGP_LAUNCH_MOVES(64, 8);
+    } else if (L.nt == 128) {
+        SGP_LAUNCH_MOVES(128, 4);
+    } else {
+        SGP_LAUNCH_MOVES(256, 2);
+    }
+#undef SGP_LAUNCH_MOVES
     return check_launch();
 }
 
@@ -755,3 +795,12 @@ extern "C" int sgp_device_info(int *sm_count, int *cc_major, int *cc_minor) {
 }
 
 extern "C" const char *sgp_version(void) { return "sgp 0.1.0 sm_100a"; }
+
+extern "C" int sgp_debug_phase_cycles(unsigned long long *h_out16, int reset) {
+    if (h_out16) CUDA_TRY(cudaMemcpyFromSymbol(h_out16, sgp_prof_cycles, sizeof(unsigned long long) * 16));
+    if (reset) {
+        unsigned long long z[16] = {0};
+        CUDA_TRY(cudaMemcpyToSymbol(sgp_prof_cycles, z, sizeof(z)));
+    }
+    return SGP_OK;
+}

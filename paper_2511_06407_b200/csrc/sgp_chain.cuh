@@ -20,14 +20,17 @@ struct ChainWS {
 struct SmemPlan {
     int CH;
     size_t off_vec, off_prm, off_stage, off_mat, bytes;
-    int mat_in_smem;
+    int nmat_smem;  // leading matrices of {H, P0, P1, W, X, T} placed in shared memory
 };
 
 __host__ __device__ inline size_t sgp_round8(size_t x) { return (x + 7) & ~size_t(7); }
 
-__host__ __device__ inline SmemPlan sgp_smem_plan(int d, int Dtot, int allow_mats) {
+// nt: threads per CTA; budget: bytes of shared memory one CTA may use (the
+// d x d matrices go to shared memory only if they fit, else to L2-resident
+// scratch, so that several chains can share an SM).
+__host__ __device__ inline SmemPlan sgp_smem_plan(int d, int Dtot, int nt, size_t budget) {
     SmemPlan s;
-    s.CH = (Dtot <= 48) ? 64 : 32;
+    s.CH = (Dtot <= 48 && nt >= 128) ? 64 : 32;
     size_t off = 0;
     off += 128 * sizeof(double);  // red + status + scalars + ints
     s.off_vec = off;
@@ -35,11 +38,16 @@ __host__ __device__ inline SmemPlan sgp_smem_plan(int d, int Dtot, int allow_mat
     s.off_prm = off;
     off += (6 * (size_t)((d + 2) / 2) + 8) * sizeof(double);
     s.off_stage = off;
-    off += ((size_t)Dtot * s.CH + 3 * SGP_NT + 8) * sizeof(double);
+    off += ((size_t)Dtot * s.CH + 3 * (size_t)nt + 8) * sizeof(double);
     s.off_mat = off;
-    size_t mats = 6 * (size_t)d * d * sizeof(double);
-    s.mat_in_smem = allow_mats && (off + mats <= 200 * 1024);
-    if (s.mat_in_smem) off += mats;
+    // H (the Jacobi working matrix) first: the serial rotation chain reads and
+    // writes it every rotation, so it is the one matrix that must not live in L2
+    const size_t mat = (size_t)d * d * sizeof(double);
+    s.nmat_smem = 0;
+    while (s.nmat_smem < 6 && off + mat <= budget) {
+        off += mat;
+        ++s.nmat_smem;
+    }
     s.bytes = off;
     return s;
 }
@@ -65,15 +73,11 @@ __device__ inline void setup_ws(ChainWS &w, EvalCtx &E, char *smem, const SmemPl
     E.stage = reinterpret_cast<double *>(smem + pl.off_stage);
     E.CH = pl.CH;
     E.S = scratch;
-    double *mb = pl.mat_in_smem ? reinterpret_cast<double *>(smem + pl.off_mat)
-                                : scratch + (size_t)F_COUNT * M.mp.ld;
     const size_t dd = (size_t)d * d;
-    w.P[0] = mb;
-    w.P[1] = mb + dd;
-    w.T = mb + 2 * dd;
-    w.W = mb + 3 * dd;
-    w.X = mb + 4 * dd;
-    w.H = mb + 5 * dd;
+    double **mats[] = {&w.H, &w.P[0], &w.P[1], &w.W, &w.X, &w.T};
+    for (int i = 0; i < 6; ++i)
+        *mats[i] = i < pl.nmat_smem ? reinterpret_cast<double *>(smem + pl.off_mat) + i * dd
+                                    : scratch + (size_t)F_COUNT * M.mp.ld + i * dd;
     if (threadIdx.x == 0) *E.status = 0;
     __syncthreads();
 }
@@ -82,13 +86,17 @@ __device__ inline void setup_ws(ChainWS &w, EvalCtx &E, char *smem, const SmemPl
 // eigendecompositions into ping-pong slot `dst`
 
 // Cold: H is consumed (becomes A); V = P[dst] from identity (metric.py:112-142).
-__device__ int eig_cold(ChainWS &w, EvalCtx &E, int d, const sgp_chain_config &cfg, int dst, int *sweeps_out) {
+__device__ __noinline__ int eig_cold(ChainWS &w, EvalCtx &E, int d, const sgp_chain_config &cfg, int dst, int *sweeps_out) {
     mat_symmetrize(w.H, d);
     const double hnorm = sqrt(frob2(w.H, d * d, E.red));
     const double tol = cfg.zeta * hnorm;
     const double skip = d ? tol / d : 0.0;
     mat_identity(w.P[dst], d);
-    int sw = jacobi_cyclic(w.H, w.P[dst], d, tol, skip, cfg.sweep_cap, E.red);
+    int sw;
+    {
+        SGP_PROF(8);
+        sw = jacobi_cyclic(w.H, w.P[dst], d, tol, skip, cfg.sweep_cap, E.red);
+    }
     if (sweeps_out) *sweeps_out = sw;
     if (sw < 0) return SGP_STATUS_JACOBI;
     for (int j = threadIdx.x; j < d; j += SGP_NT) w.lam[dst][j] = w.H[j * d + j];
@@ -104,21 +112,26 @@ __device__ int eig_cold(ChainWS &w, EvalCtx &E, int d, const sgp_chain_config &c
 
 // Warm: previous basis in P[src] (may be re-orthonormalised in place), result
 // in P[dst] (metric.py:145-185).  H is consumed.
-__device__ int eig_warm(ChainWS &w, EvalCtx &E, int d, const sgp_chain_config &cfg, int src, int dst,
+__device__ __noinline__ int eig_warm(ChainWS &w, EvalCtx &E, int d, const sgp_chain_config &cfg, int src, int dst,
                         int *sweeps_out) {
     int since = w.si[src] + 1;
     if (cfg.gs_interval && since >= cfg.gs_interval) {
+        SGP_PROF(3);
         mgs(w.P[src], d, E.red);
         since = 0;
     }
     const double hnorm = sqrt(frob2(w.H, d * d, E.red));
-    mat_mul<2>(w.X, w.P[src], w.H, d);  // X = Psi^T H
-    mat_mul<0>(w.H, w.X, w.P[src], d);  // A = X Psi
-    mat_symmetrize(w.H, d);
-    mat_copy(w.P[dst], w.P[src], d * d);  // rotations applied to Psi directly (== Psi Q)
+    {
+        SGP_PROF(4);
+        mat_mul<2>(w.X, w.P[src], w.H, d);  // X = Psi^T H
+        mat_mul<0>(w.H, w.X, w.P[src], d);  // A = X Psi
+        mat_symmetrize(w.H, d);
+        mat_copy(w.P[dst], w.P[src], d * d);  // rotations applied to Psi directly (== Psi Q)
+    }
     const double tol = cfg.zeta * hnorm;
     const double skip = d ? tol / d : 0.0;
     int sw;
+    SGP_PROF(5);
     if (cfg.warm_order == SGP_ORDER_CYCLIC)
         sw = jacobi_cyclic(w.H, w.P[dst], d, tol, skip, cfg.sweep_cap, E.red);
     else
@@ -140,7 +153,7 @@ __device__ int eig_warm(ChainWS &w, EvalCtx &E, int d, const sgp_chain_config &c
 
 struct LFDiag {
     int fp_p, fp_q, nsweep;
-    int sweeps[32];
+    int *sweeps;  // optional per-decomposition log (smem, >= fp_max_iters ints) or null
     double sweep_sum;
     int sweep_cnt;
 };
@@ -167,8 +180,9 @@ __device__ int eval_at(ChainWS &w, EvalCtx &E, const double *q, double tau, int 
 // One generalized leapfrog.  Frame = (w.q0, w.grad, per-sample S, metric slot f,
 // w.T valid for slot f); momentum in w.p.  On success the frame and w.p are
 // advanced and f may change.  Returns a status (sampler.py:209-258).
-__device__ int leapfrog_riemann(ChainWS &w, EvalCtx &E, const sgp_chain_config &cfg, double tau, int &f,
+__device__ __noinline__ int leapfrog_riemann(ChainWS &w, EvalCtx &E, const sgp_chain_config &cfg, double tau, int &f,
                                 LFDiag &dg) {
+    SGP_PROF(9);
     const int d = E.M.mp.d;
     const double eps = cfg.epsilon;
     // ---- implicit momentum half step, W2 fixed (sampler.py:216-232)
@@ -178,8 +192,9 @@ __device__ int leapfrog_riemann(ChainWS &w, EvalCtx &E, const sgp_chain_config &
     vec_axpy3(w.ph, w.p, 0.5 * eps, w.grad, w.tv, 0.5, d);
     bool conv = false;
     for (int it = 0; it < cfg.fp_max_iters; ++it) {
-        metric_w(w.W, w.X, w.bv, w.P[f], w.lam[f], w.g[f], w.T, w.ph, d, true, true);
-        eval_trace(E, w.q0, tau, w.W, w.tv);
+        { SGP_PROF(0); metric_w(w.W, w.X, w.bv, w.P[f], w.lam[f], w.g[f], w.T, w.ph, d, true, true);
+        }
+        { SGP_PROF(1); eval_trace(E, w.q0, tau, w.W, w.tv); }
         if (*E.status) return *E.status;
         vec_axpy3(w.pn, w.p, 0.5 * eps, w.grad, w.tv, 0.5, d);
         double dl = 0.0;
@@ -204,7 +219,11 @@ __device__ int leapfrog_riemann(ChainWS &w, EvalCtx &E, const sgp_chain_config &
     int prev = f, cur = f;
     conv = false;
     for (int it = 0; it < cfg.fp_max_iters; ++it) {
-        int st = eval_at(w, E, w.qc, tau, SGP_EVAL_HESSIAN);
+        int st;
+        {
+            SGP_PROF(2);
+            st = eval_at(w, E, w.qc, tau, SGP_EVAL_HESSIAN);
+        }
         if (st) return st;
         const int nxt = 1 - prev;
         int sw = 0;
@@ -212,7 +231,7 @@ __device__ int leapfrog_riemann(ChainWS &w, EvalCtx &E, const sgp_chain_config &
             st = eig_cold(w, E, d, cfg, nxt, &sw);
         else
             st = eig_warm(w, E, d, cfg, prev, nxt, &sw);
-        if (threadIdx.x == 0 && dg.nsweep < 32) dg.sweeps[dg.nsweep] = sw;
+        if (threadIdx.x == 0 && dg.sweeps && dg.nsweep < 32) dg.sweeps[dg.nsweep] = sw;
         dg.nsweep++;
         if (st) return st;
         dg.sweep_sum += sw;
@@ -291,7 +310,7 @@ __device__ double frame_kinetic(ChainWS &w, EvalCtx &E, const sgp_chain_config &
 
 // Builds the frame at w.q0: potential, gradient, per-sample S and (unless
 // Euclidean) the cold metric in slot 0 plus its T matrix (sampler.py:322-328).
-__device__ int frame_build(ChainWS &w, EvalCtx &E, const sgp_chain_config &cfg, double tau, int &f) {
+__device__ __noinline__ int frame_build(ChainWS &w, EvalCtx &E, const sgp_chain_config &cfg, double tau, int &f) {
     const int d = E.M.mp.d;
     const bool euclid = cfg.metric == SGP_METRIC_EUCLIDEAN;
     int st = eval_at(w, E, w.q0, tau,
@@ -307,7 +326,7 @@ __device__ int frame_build(ChainWS &w, EvalCtx &E, const sgp_chain_config &cfg, 
 
 // Re-derives the frame from a stored (q, psi, lam, since) without a new
 // decomposition: potential, gradient, S, g, logdet, T.
-__device__ int frame_resume(ChainWS &w, EvalCtx &E, const sgp_chain_config &cfg, double tau, const double *psi,
+__device__ __noinline__ int frame_resume(ChainWS &w, EvalCtx &E, const sgp_chain_config &cfg, double tau, const double *psi,
                             const double *lam, int since, int &f) {
     const int d = E.M.mp.d;
     int st = eval_at(w, E, w.q0, tau, SGP_EVAL_POTENTIAL | SGP_EVAL_GRADIENT);

@@ -15,7 +15,7 @@ struct EvalCtx {
 
 // Latent values and per-sample derivatives at q; returns sum_i U_i (i < N).
 // Sets DIVERGENCE for non-finite f (posterior.py:344-345).
-__device__ double eval_lik(EvalCtx &E, const double *q) {
+__device__ __noinline__ double eval_lik(EvalCtx &E, const double *q) {
     const ModelParams &mp = E.M.mp;
     const int ld = mp.ld, N = mp.N;
     const double *phi = E.M.phi;
@@ -56,7 +56,7 @@ __device__ __forceinline__ void stage_chunk(EvalCtx &E, int i0) {
 // Likelihood Hessian block sum_i tau d2_{j(a)j(b)}(i) phi_a(i) phi_b(i) for the
 // upper triangle of [0, Dtot)^2, written (and mirrored) into H (posterior.py:449-460).
 template <int J>
-__device__ void hess_lik(EvalCtx &E, double tau, double *H, int d) {
+__device__ __noinline__ void hess_lik(EvalCtx &E, double tau, double *H, int d) {
     const ModelParams &mp = E.M.mp;
     const int Dt = mp.Dtot, CH = E.CH, ld = mp.ld, D0 = mp.D[0];
     const int nb = (Dt + 1) >> 1;
@@ -169,7 +169,7 @@ __device__ void hess_lik(EvalCtx &E, double tau, double *H, int d) {
 // Per-sample quadratic forms s^(j1 j2)_i = phi_j1(x_i)^T W_blk phi_j2(x_i) and
 // their third-derivative contractions c^(j)_i (posterior.py:495-509).
 template <int J>
-__device__ void trace_lik_samples(EvalCtx &E, const double *W, int d) {
+__device__ __noinline__ void trace_lik_samples(EvalCtx &E, const double *W, int d) {
     const ModelParams &mp = E.M.mp;
     const int Dt = mp.Dtot, CH = E.CH, ld = mp.ld, D0 = mp.D[0];
     const int G = SGP_NT / CH;
@@ -231,7 +231,7 @@ __device__ void trace_lik_samples(EvalCtx &E, const double *W, int d) {
 }
 
 // out[a] = tau * sum_i phi[a,i] * S[field(j(a)), i] for a < Dtot (warp per row).
-__device__ void project_back(EvalCtx &E, double tau, int field0, int field1, double *out) {
+__device__ __noinline__ void project_back(EvalCtx &E, double tau, int field0, int field1, double *out) {
     const ModelParams &mp = E.M.mp;
     const int ld = mp.ld;
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
@@ -258,7 +258,7 @@ struct EvalOut {
     double pot, sumpot;
 };
 
-__device__ void eval_state(EvalCtx &E, const double *q, double tau, int what, double *grad, double *H, EvalOut &o) {
+__device__ __noinline__ void eval_state(EvalCtx &E, const double *q, double tau, int what, double *grad, double *H, EvalOut &o) {
     const ModelParams &mp = E.M.mp;
     const int d = mp.d;
     __syncthreads();
@@ -397,10 +397,10 @@ __device__ void eval_state(EvalCtx &E, const double *q, double tau, int what, do
             if (what & SGP_EVAL_GRADIENT) grad[pos] += u[1];
             if (what & SGP_EVAL_HESSIAN) H[pos * d + pos] += u[2];
         }
-        E.red[40] = pot;
+        E.red[72] = pot;
     }
     __syncthreads();
-    o.pot = E.red[40];
+    o.pot = E.red[72];
     if (*E.status) return;
     // finiteness checks (posterior.py:411, 437, 479)
     bool bad = false;
@@ -415,7 +415,7 @@ __device__ void eval_state(EvalCtx &E, const double *q, double tau, int what, do
 
 // t = tr(W dH/dq_i) at the point whose per-sample derivatives are in E.S
 // (posterior.py:486-542).  W must be symmetric (callers symmetrise).
-__device__ void eval_trace(EvalCtx &E, const double *q, double tau, const double *W, double *t) {
+__device__ __noinline__ void eval_trace(EvalCtx &E, const double *q, double tau, const double *W, double *t) {
     const ModelParams &mp = E.M.mp;
     const int d = mp.d;
     __syncthreads();

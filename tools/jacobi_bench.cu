@@ -1,0 +1,75 @@
+// Cycle cost per rotation of the bit-exact cyclic Jacobi (sgp_core.cuh) on a
+// near-diagonal d x d matrix, with A / V in shared or global memory.
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -o tools/jacobi_bench tools/jacobi_bench.cu
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+#include "../paper_2511_06407_b200/csrc/sgp_core.cuh"
+
+__global__ void bench(const double *A0, double *Ag, double *Vg, int d, int mode, long long *cyc, int *sw) {
+    extern __shared__ double sm[];
+    double *red = sm;
+    double *As = sm + 64;
+    double *Vs = As + d * d;
+    double *A = (mode & 1) ? Ag + blockIdx.x * d * d : As;
+    double *V = (mode & 2) ? Vg + blockIdx.x * d * d : Vs;
+    for (int i = threadIdx.x; i < d * d; i += blockDim.x) {
+        A[i] = A0[i];
+        V[i] = (i / d == i % d) ? 1.0 : 0.0;
+    }
+    __syncthreads();
+    long long t0 = clock64();
+    int s = jacobi_cyclic(A, V, d, 1e-13 * 100.0, 1e-13 * 100.0 / d, 30, red);
+    long long t1 = clock64();
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        *cyc = t1 - t0;
+        *sw = s;
+    }
+}
+
+int main(int argc, char **argv) {
+    int d = argc > 1 ? atoi(argv[1]) : 34;
+    std::vector<double> a(d * d);
+    srand(1);
+    for (int i = 0; i < d; ++i)
+        for (int j = 0; j <= i; ++j) {
+            double v = (i == j) ? 1.0 + i : 1e-3 * ((rand() % 2000) / 1000.0 - 1.0);
+            a[i * d + j] = a[j * d + i] = v;
+        }
+    double *A0, *Ag, *Vg;
+    long long *cyc, hc;
+    int *sw, hs;
+    cudaMalloc(&A0, d * d * 8);
+    cudaMalloc(&Ag, 2048 * d * d * 8);
+    cudaMalloc(&Vg, 2048 * d * d * 8);
+    cudaMalloc(&cyc, 8);
+    cudaMalloc(&sw, 4);
+    cudaMemcpy(A0, a.data(), d * d * 8, cudaMemcpyHostToDevice);
+    size_t smem = (64 + 2 * d * d) * 8;
+    cudaFuncSetAttribute(bench, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const char *names[] = {"A smem, V smem", "A glob, V smem", "A smem, V glob", "A glob, V glob"};
+    for (int nt : {32, 256}) {
+        for (int mode = 0; mode < 4; ++mode) {
+            for (int blocks : {1, 148 * 4}) {
+                bench<<<blocks, nt, smem>>>(A0, Ag, Vg, d, mode, cyc, sw);
+                cudaDeviceSynchronize();
+                cudaEvent_t e0, e1;
+                cudaEventCreate(&e0);
+                cudaEventCreate(&e1);
+                cudaEventRecord(e0);
+                bench<<<blocks, nt, smem>>>(A0, Ag, Vg, d, mode, cyc, sw);
+                cudaEventRecord(e1);
+                cudaEventSynchronize(e1);
+                float ms;
+                cudaEventElapsedTime(&ms, e0, e1);
+                cudaMemcpy(&hc, cyc, 8, cudaMemcpyDeviceToHost);
+                cudaMemcpy(&hs, sw, 4, cudaMemcpyDeviceToHost);
+                double rot = (double)hs * d * (d - 1) / 2;
+                printf("d=%d nt=%3d %-16s blocks=%4d sweeps=%d  %.0f cyc/rotation  (%.3f ms)\n", d, nt, names[mode],
+                       blocks, hs, hc / rot, ms);
+            }
+        }
+    }
+    return 0;
+}
