@@ -372,7 +372,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--chains", type=int, default=0, help="chains per GPU (default SMs x chains-per-sm)")
-    ap.add_argument("--chains-per-sm", type=int, default=1)
+    ap.add_argument("--chains-per-sm", type=int, default=12)
     ap.add_argument("--warm-order", default="cyclic", choices=["cyclic", "parallel"])
     ap.add_argument("--ref-leapfrogs", type=int, default=20)
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -170,6 +170,9 @@ extern "C" int sgp_model_create(const sgp_model_desc *desc, sgp_model **out) {
         mp.fstart[1] = pos;
     }
     mp.Dtot = pos;
+    mp.Dp0 = (mp.D[0] + 3) & ~3;
+    mp.Dp1 = (mp.D[1] + 3) & ~3;
+    mp.Dp = mp.Dp0 + mp.Dp1;
     for (int s = 0; s < 3; ++s) {
         if (desc->hyper_sampled[s]) {
             mp.hpos[s] = pos++;
@@ -226,7 +229,7 @@ extern "C" int sgp_model_features(const sgp_model *m, int j) {
     return m->dev.mp.D[j];
 }
 extern "C" size_t sgp_scratch_doubles(const sgp_model *m) {
-    return m ? sgp_scratch_per_chain(m->dev.mp.ld, m->dev.mp.d) : 0;
+    return m ? sgp_scratch_per_chain(m->dev.mp.ld, m->dev.mp.d, m->dev.mp.Dp) : 0;
 }
 
 __global__ void k_phi_out(const double *phi, int ld, int N, int a0, int Dj, double *out) {
@@ -271,7 +274,7 @@ __global__ void __launch_bounds__(SGP_MAX_NT) k_eval(ModelDev M, SmemPlan pl, co
 }
 
 static SmemPlan plan_for(const sgp_model *m, int allow_mats) {
-    return sgp_smem_plan(m->dev.mp.d, m->dev.mp.Dtot, SGP_MAX_NT, allow_mats ? 200 * 1024 : 0);
+    return sgp_smem_plan(m->dev.mp.d, m->dev.mp.Dp, SGP_MAX_NT, allow_mats ? 200 * 1024 : 16 * 1024);
 }
 
 // Launch shape of the fused chain kernel: threads per CTA and the number of
@@ -292,9 +295,13 @@ static ChainLaunch chain_launch(const sgp_model *m) {
     }
     ChainLaunch L;
     L.nt = nt;
-    L.per_sm = nt == 32 ? 16 : (nt == 64 ? 8 : (nt == 128 ? 4 : 2));
+    L.per_sm = nt == 32 ? 12 : (nt == 64 ? 6 : (nt == 128 ? 4 : 2));
+    const char *eps = getenv("SGP_CHAINS_PER_SM");
+    if (eps && atoi(eps) > 0) L.per_sm = atoi(eps);
+    const char *ech = getenv("SGP_STAGE_CH");
+    const int ch = ech ? atoi(ech) : 0;
     const size_t budget = (227 * 1024) / L.per_sm - 1024;
-    L.pl = sgp_smem_plan(m->dev.mp.d, m->dev.mp.Dtot, nt, budget);
+    L.pl = sgp_smem_plan(m->dev.mp.d, m->dev.mp.Dp, nt, budget, (ch == 16 || ch == 32 || ch == 64) ? ch : 0);
     return L;
 }
 
@@ -402,7 +409,7 @@ __global__ void __launch_bounds__(SGP_MAX_NT) k_eigh_cold(int d, const double *H
     const double hnorm = sqrt(frob2(A, d * d, red));
     const double tol = zeta * hnorm;
     const double skip = d ? tol / d : 0.0;
-    int sw = jacobi_cyclic(A, V, d, tol, skip, cap, red);
+    int sw = jacobi_cyclic(A, V, d, tol, skip, cap, red, tmp + gridDim.x * dd + z * sgp_jacobi_log_doubles(d));
     for (int j = threadIdx.x; j < d; j += SGP_NT) lam[(size_t)z * d + j] = A[j * d + j];
     if (threadIdx.x == 0) sweeps[z] = sw;
 }
@@ -411,7 +418,7 @@ extern "C" int sgp_eigh_cold(int Z, int d, const double *d_h, double zeta, int c
                              int *d_sweeps, void *stream) {
     if (Z < 1 || d < 1 || !d_h || !d_lam || !d_psi || !d_sweeps) return SGP_EINVAL;
     double *tmp = nullptr;
-    CUDA_TRY(cudaMallocAsync(&tmp, sizeof(double) * Z * (size_t)d * d, S(stream)));
+    CUDA_TRY(cudaMallocAsync(&tmp, sizeof(double) * Z * ((size_t)d * d + sgp_jacobi_log_doubles(d)), S(stream)));
     k_eigh_cold<<<Z, SGP_MAX_NT, 0, S(stream)>>>(d, d_h, zeta, cap, d_lam, d_psi, d_sweeps, tmp);
     int rc = check_launch();
     cudaFreeAsync(tmp, S(stream));
@@ -443,7 +450,8 @@ __global__ void __launch_bounds__(SGP_MAX_NT) k_eigh_warm(int d, const double *H
     mat_symmetrize(A, d);
     const double tol = zeta * hnorm;
     const double skip = d ? tol / d : 0.0;
-    int sw = order == SGP_ORDER_CYCLIC ? jacobi_cyclic(A, V, d, tol, skip, cap, red)
+    int sw = order == SGP_ORDER_CYCLIC
+                 ? jacobi_cyclic(A, V, d, tol, skip, cap, red, tmp + 2 * gridDim.x * dd + z * sgp_jacobi_log_doubles(d))
                                        : jacobi_parallel(A, V, d, tol, skip, cap, red, prm);
     for (int j = threadIdx.x; j < d; j += SGP_NT) lam[(size_t)z * d + j] = A[j * d + j];
     if (threadIdx.x == 0) {
@@ -458,7 +466,7 @@ extern "C" int sgp_eigh_warm(int Z, int d, const double *d_h, const double *d_ps
     if (Z < 1 || d < 1 || !d_h || !d_psi_prev || !d_since_prev || !d_lam || !d_psi || !d_since || !d_sweeps)
         return SGP_EINVAL;
     double *tmp = nullptr;
-    CUDA_TRY(cudaMallocAsync(&tmp, sizeof(double) * 2 * Z * (size_t)d * d, S(stream)));
+    CUDA_TRY(cudaMallocAsync(&tmp, sizeof(double) * Z * (2 * (size_t)d * d + sgp_jacobi_log_doubles(d)), S(stream)));
     size_t smem = (6 * (size_t)((d + 2) / 2) + 8) * sizeof(double);
     int rc = launch_prep(k_eigh_warm, smem);
     if (rc) return rc;
@@ -771,9 +779,9 @@ extern "C" int sgp_run_moves(const sgp_model *m, const sgp_chain_config *cfg, co
     k_run_moves<NT_, MB_><<<st->n_chains, NT_, L.pl.bytes, S(stream)>>>(m->dev, L.pl, *cfg, *st, moves,    \
                                                                         move_offset, d_z, d_logu, *rec, spc)
     if (L.nt == 32) {
-        SGP_LAUNCH_MOVES(32, 16);
+        SGP_LAUNCH_MOVES(32, 12);
     } else if (L.nt == 64) {
-        SGP_LAUNCH_MOVES(64, 8);
+        SGP_LAUNCH_MOVES(64, 6);
     } else if (L.nt == 128) {
         SGP_LAUNCH_MOVES(128, 4);
     } else {

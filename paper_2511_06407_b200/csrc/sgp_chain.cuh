@@ -12,54 +12,70 @@ struct ChainWS {
     double *q0, *qc, *qn, *qs, *p, *ph, *pn, *v0, *grad, *tv, *bv, *tmp;
     double *lam[2], *g[2];
     double *prm;   // parallel-Jacobi parameters
+    double *jlog;  // rotation log of the cyclic Jacobi (scratch)
     double *sc;    // shared scalars: [0..1] logdet[2], [2] pot, [3] su, [4] pot_start
     int *si;       // shared ints: [0..1] since[2]
 };
 
 // Shared-memory layout (host and device compute it identically).
+// Matrices, in placement priority: H (the serial Jacobi works in it every
+// rotation), Wp (padded contraction matrix read by every trace tile), W, P0,
+// P1, X, T.  Those that do not fit the per-CTA budget live in the chain's
+// L2-resident scratch slice, so several chains can share an SM.
+#define SGP_NMAT 7
 struct SmemPlan {
     int CH;
-    size_t off_vec, off_prm, off_stage, off_mat, bytes;
-    int nmat_smem;  // leading matrices of {H, P0, P1, W, X, T} placed in shared memory
+    size_t off_vec, off_prm, off_stage, bytes;
+    size_t off_mat[SGP_NMAT];  // byte offset in smem, or (size_t)-1 if in scratch
 };
 
-__host__ __device__ inline size_t sgp_round8(size_t x) { return (x + 7) & ~size_t(7); }
+__host__ __device__ inline size_t sgp_round2(size_t x) { return (x + 1) & ~size_t(1); }
 
-// nt: threads per CTA; budget: bytes of shared memory one CTA may use (the
-// d x d matrices go to shared memory only if they fit, else to L2-resident
-// scratch, so that several chains can share an SM).
-__host__ __device__ inline SmemPlan sgp_smem_plan(int d, int Dtot, int nt, size_t budget) {
+__host__ __device__ inline size_t sgp_stage_doubles(int Dp, int CH) {
+    return sgp_round2((size_t)CH * (Dp + 2) + 3 * (size_t)CH + (size_t)(Dp / 4) * CH * 3 + 2);
+}
+
+__host__ __device__ inline size_t sgp_mat_doubles(int i, int d, int Dp) {
+    return i == 1 ? (size_t)Dp * Dp : (size_t)d * d;
+}
+
+__host__ __device__ inline SmemPlan sgp_smem_plan(int d, int Dp, int nt, size_t budget, int ch = 0) {
     SmemPlan s;
-    s.CH = (Dtot <= 48 && nt >= 128) ? 64 : 32;
+    s.CH = ch > 0 ? ch : (nt <= 64 ? 16 : ((Dp <= 48 && nt >= 128) ? 64 : 32));
     size_t off = 0;
     off += 128 * sizeof(double);  // red + status + scalars + ints
     s.off_vec = off;
-    off += sgp_round8(16 * (size_t)d + 8) * sizeof(double);
+    off += sgp_round2(16 * (size_t)d + 8) * sizeof(double);
     s.off_prm = off;
-    off += (6 * (size_t)((d + 2) / 2) + 8) * sizeof(double);
+    off += sgp_round2(6 * (size_t)((d + 2) / 2) + 8) * sizeof(double);
     s.off_stage = off;
-    off += ((size_t)Dtot * s.CH + 3 * (size_t)nt + 8) * sizeof(double);
-    s.off_mat = off;
-    // H (the Jacobi working matrix) first: the serial rotation chain reads and
-    // writes it every rotation, so it is the one matrix that must not live in L2
-    const size_t mat = (size_t)d * d * sizeof(double);
-    s.nmat_smem = 0;
-    while (s.nmat_smem < 6 && off + mat <= budget) {
-        off += mat;
-        ++s.nmat_smem;
+    off += sgp_stage_doubles(Dp, s.CH) * sizeof(double);
+    for (int i = 0; i < SGP_NMAT; ++i) {
+        const size_t m = sgp_round2(sgp_mat_doubles(i, d, Dp)) * sizeof(double);
+        if (off + m <= budget) {
+            s.off_mat[i] = off;
+            off += m;
+        } else {
+            s.off_mat[i] = (size_t)-1;
+        }
     }
     s.bytes = off;
     return s;
 }
 
-// per-chain scratch (doubles): per-sample fields + 6 d x d matrices + q_start
-__host__ __device__ inline size_t sgp_scratch_per_chain(int ld, int d) {
-    return (size_t)F_COUNT * ld + 6 * (size_t)d * d + 2 * (size_t)d + 64;
+// per-chain scratch (doubles): per-sample fields, the 7 matrices, Jacobi log
+__host__ __device__ inline size_t sgp_scratch_mat_offset(int ld, int d, int Dp, int i) {
+    size_t off = (size_t)F_COUNT * ld;
+    for (int k = 0; k < i; ++k) off += sgp_round2(sgp_mat_doubles(k, d, Dp));
+    return off;
+}
+__host__ __device__ inline size_t sgp_scratch_per_chain(int ld, int d, int Dp) {
+    return sgp_scratch_mat_offset(ld, d, Dp, SGP_NMAT) + sgp_jacobi_log_doubles(d) + 2 * (size_t)d + 64;
 }
 
 __device__ inline void setup_ws(ChainWS &w, EvalCtx &E, char *smem, const SmemPlan &pl, const ModelDev &M,
                                 double *scratch) {
-    const int d = M.mp.d;
+    const int d = M.mp.d, Dp = M.mp.Dp, ld = M.mp.ld;
     E.M = M;
     E.red = reinterpret_cast<double *>(smem);
     E.status = reinterpret_cast<int *>(smem + 64 * sizeof(double));
@@ -73,11 +89,11 @@ __device__ inline void setup_ws(ChainWS &w, EvalCtx &E, char *smem, const SmemPl
     E.stage = reinterpret_cast<double *>(smem + pl.off_stage);
     E.CH = pl.CH;
     E.S = scratch;
-    const size_t dd = (size_t)d * d;
-    double **mats[] = {&w.H, &w.P[0], &w.P[1], &w.W, &w.X, &w.T};
-    for (int i = 0; i < 6; ++i)
-        *mats[i] = i < pl.nmat_smem ? reinterpret_cast<double *>(smem + pl.off_mat) + i * dd
-                                    : scratch + (size_t)F_COUNT * M.mp.ld + i * dd;
+    double **mats[SGP_NMAT] = {&w.H, &E.wp, &w.W, &w.P[0], &w.P[1], &w.X, &w.T};
+    for (int i = 0; i < SGP_NMAT; ++i)
+        *mats[i] = pl.off_mat[i] != (size_t)-1 ? reinterpret_cast<double *>(smem + pl.off_mat[i])
+                                               : scratch + sgp_scratch_mat_offset(ld, d, Dp, i);
+    w.jlog = scratch + sgp_scratch_mat_offset(ld, d, Dp, SGP_NMAT);
     if (threadIdx.x == 0) *E.status = 0;
     __syncthreads();
 }
@@ -95,7 +111,7 @@ __device__ __noinline__ int eig_cold(ChainWS &w, EvalCtx &E, int d, const sgp_ch
     int sw;
     {
         SGP_PROF(8);
-        sw = jacobi_cyclic(w.H, w.P[dst], d, tol, skip, cfg.sweep_cap, E.red);
+        sw = jacobi_cyclic(w.H, w.P[dst], d, tol, skip, cfg.sweep_cap, E.red, w.jlog);
     }
     if (sweeps_out) *sweeps_out = sw;
     if (sw < 0) return SGP_STATUS_JACOBI;
@@ -133,7 +149,7 @@ __device__ __noinline__ int eig_warm(ChainWS &w, EvalCtx &E, int d, const sgp_ch
     int sw;
     SGP_PROF(5);
     if (cfg.warm_order == SGP_ORDER_CYCLIC)
-        sw = jacobi_cyclic(w.H, w.P[dst], d, tol, skip, cfg.sweep_cap, E.red);
+        sw = jacobi_cyclic(w.H, w.P[dst], d, tol, skip, cfg.sweep_cap, E.red, w.jlog);
     else
         sw = jacobi_parallel(w.H, w.P[dst], d, tol, skip, cfg.sweep_cap, E.red, w.prm);
     if (sweeps_out) *sweeps_out = sw;

@@ -7,7 +7,8 @@
 struct EvalCtx {
     ModelDev M;
     double *S;      // per-sample fields, F_COUNT x ld (global scratch)
-    double *stage;  // smem staging for a chunk of samples: Dtot*CH + 3*CH
+    double *stage;  // smem staging of a chunk of samples (see stage_chunk_sm)
+    double *wp;     // padded Dp x Dp copy of the contraction matrix
     int CH;         // samples per chunk
     double *red;    // smem reduction scratch (>= 64 doubles)
     int *status;    // smem status word
@@ -247,6 +248,227 @@ __device__ __noinline__ void project_back(EvalCtx &E, double tau, int field0, in
     __syncthreads();
 }
 
+
+// ---------------------------------------------------------------------------
+// Register-tiled likelihood contractions.  A chunk of CH samples of Phi is
+// staged sample-major with each function's feature block padded to a multiple
+// of 4: stage[ii*SP + a'], SP = Dp + 2.  4x4 register tiles then give 16
+// independent FMAs per 8 operand loads (two 16-byte shared loads per four
+// operands), instead of one dependent FMA per load.
+
+__device__ __forceinline__ int pad_to_coord(const ModelParams &mp, int a) {
+    if (a < mp.Dp0) return a < mp.D[0] ? a : -1;
+    const int b = a - mp.Dp0;
+    return b < mp.D[1] ? mp.D[0] + b : -1;
+}
+
+__device__ __forceinline__ void stage_chunk_sm(EvalCtx &E, int i0) {
+    const ModelParams &mp = E.M.mp;
+    const int CH = E.CH, SP = mp.Dp + 2, ld = mp.ld;
+    for (int idx = threadIdx.x; idx < mp.Dp * CH; idx += SGP_NT) {
+        const int a = idx / CH, ii = idx - a * CH;
+        const int c = pad_to_coord(mp, a);
+        const int i = i0 + ii;
+        E.stage[ii * SP + a] = (c >= 0 && i < mp.N) ? E.M.phi[(size_t)c * ld + i] : 0.0;
+    }
+}
+
+__device__ __forceinline__ void load4(const double *p, double *x) {
+    const double2 a = reinterpret_cast<const double2 *>(p)[0];
+    const double2 b = reinterpret_cast<const double2 *>(p)[1];
+    x[0] = a.x;
+    x[1] = a.y;
+    x[2] = b.x;
+    x[3] = b.y;
+}
+
+// upper-triangle tile index -> (bi, bj), bi <= bj, of an nb x nb tile grid
+__device__ __forceinline__ void tri_decode(int t, int nb, int &bi, int &bj) {
+    bi = 0;
+    while (t >= nb - bi) {
+        t -= nb - bi;
+        ++bi;
+    }
+    bj = bi + t;
+}
+
+// H[a][b] (+mirror) = tau sum_i d2_{j(a)j(b)}(i) phi_a(i) phi_b(i), a <= b < Dtot
+// (posterior.py:449-460).  H must be zero on entry for the likelihood block.
+template <int J>
+__device__ __noinline__ void hess_lik_tiled(EvalCtx &E, double tau, double *H, int d) {
+    const ModelParams &mp = E.M.mp;
+    const int CH = E.CH, SP = mp.Dp + 2, nb = mp.Dp >> 2, ld = mp.ld;
+    const int ntile = nb * (nb + 1) / 2;
+    double *wst = E.stage + CH * SP;
+    const int R = max(1, min(8, SGP_NT / max(1, ntile)));
+    const int items = ntile * R;
+    for (int base = 0; base < items; base += 2 * SGP_NT) {
+        int a0[2], b0[2], rep[2], nmine = 0;
+        double acc[2][16];
+        for (int s = 0; s < 2; ++s) {
+            const int it = base + threadIdx.x + s * SGP_NT;
+            if (it < items) {
+                int bi, bj;
+                tri_decode(it % ntile, nb, bi, bj);
+                a0[nmine] = 4 * bi;
+                b0[nmine] = 4 * bj;
+                rep[nmine] = it / ntile;
+                ++nmine;
+            }
+        }
+#pragma unroll
+        for (int s = 0; s < 2; ++s)
+#pragma unroll
+            for (int e = 0; e < 16; ++e) acc[s][e] = 0.0;
+        for (int i0 = 0; i0 < mp.N; i0 += CH) {
+            __syncthreads();
+            stage_chunk_sm(E, i0);
+            for (int ii = threadIdx.x; ii < CH; ii += SGP_NT) {
+                const int i = i0 + ii;
+                const bool ok = i < mp.N;
+                wst[ii] = ok ? tau * E.S[F_D2_00 * ld + i] : 0.0;
+                if (J == 2) {
+                    wst[CH + ii] = ok ? tau * E.S[F_D2_01 * ld + i] : 0.0;
+                    wst[2 * CH + ii] = ok ? tau * E.S[F_D2_11 * ld + i] : 0.0;
+                }
+            }
+            __syncthreads();
+#pragma unroll
+            for (int s = 0; s < 2; ++s) {
+                if (s >= nmine) break;
+                const int ja = J == 2 && a0[s] >= mp.Dp0, jb = J == 2 && b0[s] >= mp.Dp0;
+                const double *wk = wst + (ja + jb) * CH;
+                for (int ii = rep[s]; ii < CH; ii += R) {
+                    double xa[4], xb[4];
+                    load4(E.stage + ii * SP + a0[s], xa);
+                    load4(E.stage + ii * SP + b0[s], xb);
+                    const double w = wk[ii];
+#pragma unroll
+                    for (int v = 0; v < 4; ++v) xb[v] *= w;
+#pragma unroll
+                    for (int u = 0; u < 4; ++u)
+#pragma unroll
+                        for (int v = 0; v < 4; ++v) acc[s][u * 4 + v] += xa[u] * xb[v];
+                }
+            }
+        }
+        // ordered reduction over sample replicas, then mirror
+        for (int r = 0; r < R; ++r) {
+            __syncthreads();
+            for (int s = 0; s < nmine; ++s) {
+                if (rep[s] != r) continue;
+                for (int u = 0; u < 4; ++u) {
+                    const int a = pad_to_coord(mp, a0[s] + u);
+                    if (a < 0) continue;
+                    for (int v = 0; v < 4; ++v) {
+                        if (a0[s] + u > b0[s] + v) continue;
+                        const int b = pad_to_coord(mp, b0[s] + v);
+                        if (b < 0) continue;
+                        double val = acc[s][u * 4 + v];
+                        if (r > 0) val += H[a * d + b];
+                        H[a * d + b] = val;
+                        H[b * d + a] = val;
+                    }
+                }
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// Wp[a'][b'] = W[coord(a')][coord(b')] (0 on padding), symmetrised.
+__device__ void build_wpad(const ModelParams &mp, const double *W, int d, double *Wp) {
+    const int Dp = mp.Dp;
+    for (int idx = threadIdx.x; idx < Dp * Dp; idx += SGP_NT) {
+        const int a = idx / Dp, b = idx - a * Dp;
+        const int ca = pad_to_coord(mp, a), cb = pad_to_coord(mp, b);
+        Wp[idx] = (ca >= 0 && cb >= 0) ? 0.5 * (W[ca * d + cb] + W[cb * d + ca]) : 0.0;
+    }
+    __syncthreads();
+}
+
+// s^(j1 j2)_i = phi_j1(x_i)^T W phi_j2(x_i) per sample, contracted with d3 into
+// c^(j)_i (posterior.py:495-509).  Tiles: 4 samples x 4 columns b of Y = Phi W.
+template <int J>
+__device__ __noinline__ void trace_lik_tiled(EvalCtx &E, const double *Wp) {
+    const ModelParams &mp = E.M.mp;
+    const int CH = E.CH, SP = mp.Dp + 2, Dp = mp.Dp, nb = Dp >> 2, ld = mp.ld;
+    const int ngrp = CH >> 2, tiles = ngrp * nb;
+    double *part = E.stage + CH * SP + 3 * CH;  // nb * CH * 3
+    for (int i0 = 0; i0 < mp.N; i0 += CH) {
+        __syncthreads();
+        stage_chunk_sm(E, i0);
+        __syncthreads();
+        for (int t = threadIdx.x; t < tiles; t += SGP_NT) {
+            const int g = t / nb, bt = t - g * nb;
+            const int ii0 = 4 * g, b0 = 4 * bt;
+            double y0[16], y1[16];
+#pragma unroll
+            for (int e = 0; e < 16; ++e) y0[e] = y1[e] = 0.0;
+            for (int a = 0; a < mp.Dp0; ++a) {
+                double w[4];
+                load4(Wp + a * Dp + b0, w);
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const double x = E.stage[(ii0 + u) * SP + a];
+#pragma unroll
+                    for (int v = 0; v < 4; ++v) y0[u * 4 + v] += x * w[v];
+                }
+            }
+            if (J == 2) {
+                for (int a = mp.Dp0; a < Dp; ++a) {
+                    double w[4];
+                    load4(Wp + a * Dp + b0, w);
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const double x = E.stage[(ii0 + u) * SP + a];
+#pragma unroll
+                        for (int v = 0; v < 4; ++v) y1[u * 4 + v] += x * w[v];
+                    }
+                }
+            }
+            const bool jb = J == 2 && b0 >= mp.Dp0;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                double xb[4];
+                load4(E.stage + (ii0 + u) * SP + b0, xb);
+                double p0 = 0.0, p1 = 0.0;
+#pragma unroll
+                for (int v = 0; v < 4; ++v) {
+                    p0 += y0[u * 4 + v] * xb[v];
+                    p1 += y1[u * 4 + v] * xb[v];
+                }
+                double *pp = part + ((size_t)bt * CH + ii0 + u) * 3;
+                pp[0] = jb ? 0.0 : p0;
+                pp[1] = jb ? p0 : p1;
+                pp[2] = jb ? p1 : 0.0;
+            }
+        }
+        __syncthreads();
+        for (int ii = threadIdx.x; ii < CH; ii += SGP_NT) {
+            const int i = i0 + ii;
+            if (i >= mp.N) continue;
+            double s00 = 0.0, sx = 0.0, s11 = 0.0;
+            for (int bt = 0; bt < nb; ++bt) {
+                const double *pp = part + ((size_t)bt * CH + ii) * 3;
+                s00 += pp[0];
+                sx += pp[1];
+                s11 += pp[2];
+            }
+            if (J == 1) {
+                E.S[F_C0 * ld + i] = E.S[F_D3_000 * ld + i] * s00;
+            } else {
+                const double t001 = E.S[F_D3_001 * ld + i], t011 = E.S[F_D3_011 * ld + i];
+                const double t111 = E.S[F_D3_111 * ld + i];
+                // d3[0,0,0] is structurally zero for the mean/variance likelihood
+                E.S[F_C0 * ld + i] = t001 * sx + t011 * s11;
+                E.S[F_C1 * ld + i] = t001 * s00 + t011 * sx + t111 * s11;
+            }
+        }
+    }
+    __syncthreads();
+}
+
 // ---------------------------------------------------------------------------
 // Full evaluation at q.  what: SGP_EVAL_* bits.  Writes *pot (potential),
 // *sumpot (sum_i U_i), grad[d], H[d*d] as requested.  Status via E.status.
@@ -316,9 +538,9 @@ __device__ __noinline__ void eval_state(EvalCtx &E, const double *q, double tau,
         __syncthreads();
         if (lik_on) {
             if (mp.J == 1)
-                hess_lik<1>(E, tau, H, d);
+                hess_lik_tiled<1>(E, tau, H, d);
             else
-                hess_lik<2>(E, tau, H, d);
+                hess_lik_tiled<2>(E, tau, H, d);
         }
         __syncthreads();
     }
@@ -425,10 +647,11 @@ __device__ __noinline__ void eval_trace(EvalCtx &E, const double *q, double tau,
         return;
     }
     if (tau != 0.0) {
+        build_wpad(mp, W, d, E.wp);
         if (mp.J == 1)
-            trace_lik_samples<1>(E, W, d);
+            trace_lik_tiled<1>(E, E.wp);
         else
-            trace_lik_samples<2>(E, W, d);
+            trace_lik_tiled<2>(E, E.wp);
         project_back(E, tau, F_C0, F_C1, t);
         for (int a = mp.Dtot + threadIdx.x; a < d; a += SGP_NT) t[a] = 0.0;
     } else {

@@ -20,7 +20,7 @@ __global__ void bench(const double *A0, double *Ag, double *Vg, int d, int mode,
     }
     __syncthreads();
     long long t0 = clock64();
-    int s = jacobi_cyclic(A, V, d, 1e-13 * 100.0, 1e-13 * 100.0 / d, 30, red);
+    int s = jacobi_cyclic(A, V, d, 1e-13 * 100.0, 1e-13 * 100.0 / d, 30, red, Vg + 1024 * d * d + blockIdx.x * sgp_jacobi_log_doubles(d));
     long long t1 = clock64();
     if (threadIdx.x == 0 && blockIdx.x == 0) {
         *cyc = t1 - t0;
@@ -42,7 +42,7 @@ int main(int argc, char **argv) {
     int *sw, hs;
     cudaMalloc(&A0, d * d * 8);
     cudaMalloc(&Ag, 2048 * d * d * 8);
-    cudaMalloc(&Vg, 2048 * d * d * 8);
+    cudaMalloc(&Vg, 2048 * (d * d + sgp_jacobi_log_doubles(d)) * 8);
     cudaMalloc(&cyc, 8);
     cudaMalloc(&sw, 4);
     cudaMemcpy(A0, a.data(), d * d * 8, cudaMemcpyHostToDevice);
