@@ -287,7 +287,7 @@ struct ChainLaunch {
     SmemPlan pl;
 };
 static ChainLaunch chain_launch(const sgp_model *m) {
-    int nt = m->dev.mp.d <= 64 ? 32 : 256;
+    int nt = m->dev.mp.d <= 64 ? 64 : 256;
     const char *env = getenv("SGP_CHAIN_THREADS");
     if (env) {
         int v = atoi(env);
