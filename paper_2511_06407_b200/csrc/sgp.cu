@@ -16,7 +16,7 @@ extern __shared__ __align__(16) char sgp_smem[];
 
 struct sgp_model {
     ModelDev dev;
-    double *d_phi, *d_y, *d_cw, *d_prec, *d_mean;
+    double *d_phi, *d_phis, *d_y, *d_cw, *d_prec, *d_mean;
     int8_t *d_ckind;
 };
 
@@ -78,6 +78,20 @@ __global__ void k_assemble_phi(const double *__restrict__ x, int N, int P, int l
             }
         }
         phi[(size_t)a * ld + i] = v;
+    }
+}
+
+// sample-major, function-padded copy used by the tiled contractions
+__global__ void k_pad_phi(const double *__restrict__ phi, ModelParams mp, double *__restrict__ phis) {
+    const int total = mp.ld * mp.Dp;
+    for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += gridDim.x * blockDim.x) {
+        const int i = idx / mp.Dp, a = idx - i * mp.Dp;
+        int c;
+        if (a < mp.Dp0)
+            c = a < mp.D[0] ? a : -1;
+        else
+            c = a - mp.Dp0 < mp.D[1] ? mp.D[0] + a - mp.Dp0 : -1;
+        phis[idx] = (c >= 0 && i < mp.N) ? phi[(size_t)c * mp.ld + i] : 0.0;
     }
 }
 
@@ -199,10 +213,14 @@ extern "C" int sgp_model_create(const sgp_model_desc *desc, sgp_model **out) {
     dim3 grid((ld + 255) / 256, Dt);
     k_assemble_phi<<<grid, 256>>>(d_x, N, P, ld, d_rows, Dt, m->d_phi);
     CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaMalloc(&m->d_phis, sizeof(double) * (size_t)ld * mp.Dp));
+    k_pad_phi<<<(ld * mp.Dp + 255) / 256, 256>>>(m->d_phi, mp, m->d_phis);
+    CUDA_TRY(cudaGetLastError());
     CUDA_TRY(cudaDeviceSynchronize());
     cudaFree(d_x);
     cudaFree(d_rows);
     m->dev.phi = m->d_phi;
+    m->dev.phis = m->d_phis;
     m->dev.y = m->d_y;
     m->dev.ckind = m->d_ckind;
     m->dev.cw = m->d_cw;
@@ -213,6 +231,7 @@ extern "C" int sgp_model_create(const sgp_model_desc *desc, sgp_model **out) {
 extern "C" int sgp_model_destroy(sgp_model *m) {
     if (!m) return SGP_OK;
     cudaFree(m->d_phi);
+    cudaFree(m->d_phis);
     cudaFree(m->d_y);
     cudaFree(m->d_cw);
     cudaFree(m->d_ckind);

@@ -32,7 +32,7 @@ struct SmemPlan {
 __host__ __device__ inline size_t sgp_round2(size_t x) { return (x + 1) & ~size_t(1); }
 
 __host__ __device__ inline size_t sgp_stage_doubles(int Dp, int CH) {
-    return sgp_round2((size_t)CH * (Dp + 2) + 3 * (size_t)CH + (size_t)(Dp / 4) * CH * 3 + 2);
+    return sgp_round2(2 * ((size_t)CH * (Dp + 2) + 3 * (size_t)CH) + (size_t)(Dp / 4) * CH * 3 + 2);
 }
 
 __host__ __device__ inline size_t sgp_mat_doubles(int i, int d, int Dp) {

@@ -42,195 +42,6 @@ __device__ __noinline__ double eval_lik(EvalCtx &E, const double *q) {
     return block_sum(su, E.red);
 }
 
-// ---------------------------------------------------------------------------
-// staging of a chunk of samples: stage[a*CH + ii] = phi[a, i0+ii]
-__device__ __forceinline__ void stage_chunk(EvalCtx &E, int i0) {
-    const ModelParams &mp = E.M.mp;
-    const int CH = E.CH, ld = mp.ld;
-    for (int idx = threadIdx.x; idx < mp.Dtot * CH; idx += SGP_NT) {
-        const int a = idx / CH, ii = idx - a * CH;
-        const int i = i0 + ii;
-        E.stage[idx] = (i < ld) ? E.M.phi[a * ld + i] : 0.0;
-    }
-}
-
-// Likelihood Hessian block sum_i tau d2_{j(a)j(b)}(i) phi_a(i) phi_b(i) for the
-// upper triangle of [0, Dtot)^2, written (and mirrored) into H (posterior.py:449-460).
-template <int J>
-__device__ __noinline__ void hess_lik(EvalCtx &E, double tau, double *H, int d) {
-    const ModelParams &mp = E.M.mp;
-    const int Dt = mp.Dtot, CH = E.CH, ld = mp.ld, D0 = mp.D[0];
-    const int nb = (Dt + 1) >> 1;
-    const int ntu = nb * (nb + 1) / 2;  // upper-triangle 2x2 tiles
-    double *wst = E.stage + Dt * CH;    // 3*CH weights
-    int R = 1;
-    if (ntu * 2 <= SGP_NT) R = min(4, SGP_NT / ntu);
-    const int per_pass = (R > 1) ? ntu : SGP_NT * 4;
-    for (int base = 0; base < ntu; base += per_pass) {
-        double acc[4][4];
-        int tiles[4];
-        int nmine = 0, rep = 0;
-        if (R > 1) {
-            if ((int)threadIdx.x < R * ntu) {
-                tiles[0] = threadIdx.x % ntu;
-                rep = threadIdx.x / ntu;
-                nmine = 1;
-            }
-        } else {
-            for (int s = 0; s < 4; ++s) {
-                int t = base + threadIdx.x + s * SGP_NT;
-                if (t < ntu) tiles[nmine++] = t;
-            }
-        }
-        int ti[4], tj[4];
-        for (int s = 0; s < nmine; ++s) {
-            // linear upper-triangle index -> (bi, bj), bi <= bj
-            int t = tiles[s], bi = 0;
-            while (t >= nb - bi) {
-                t -= nb - bi;
-                ++bi;
-            }
-            ti[s] = bi * 2;
-            tj[s] = (bi + t) * 2;
-            for (int e = 0; e < 4; ++e) acc[s][e] = 0.0;
-        }
-        for (int i0 = 0; i0 < ld; i0 += CH) {
-            __syncthreads();
-            stage_chunk(E, i0);
-            for (int ii = threadIdx.x; ii < CH; ii += SGP_NT) {
-                const int i = i0 + ii;
-                const bool ok = i < mp.N;
-                wst[ii] = ok ? tau * E.S[F_D2_00 * ld + i] : 0.0;
-                if (J == 2) {
-                    wst[CH + ii] = ok ? tau * E.S[F_D2_01 * ld + i] : 0.0;
-                    wst[2 * CH + ii] = ok ? tau * E.S[F_D2_11 * ld + i] : 0.0;
-                }
-            }
-            __syncthreads();
-            for (int s = 0; s < nmine; ++s) {
-                const int a0 = ti[s], b0 = tj[s];
-                const int a1 = min(a0 + 1, Dt - 1), b1 = min(b0 + 1, Dt - 1);
-                const double *pa0 = E.stage + a0 * CH, *pa1 = E.stage + a1 * CH;
-                const double *pb0 = E.stage + b0 * CH, *pb1 = E.stage + b1 * CH;
-                if (J == 1) {
-                    double c00 = acc[s][0], c01 = acc[s][1], c10 = acc[s][2], c11 = acc[s][3];
-                    for (int ii = rep; ii < CH; ii += R) {
-                        const double w = wst[ii];
-                        const double x0 = pa0[ii] * w, x1 = pa1[ii] * w;
-                        const double y0 = pb0[ii], y1 = pb1[ii];
-                        c00 += x0 * y0;
-                        c01 += x0 * y1;
-                        c10 += x1 * y0;
-                        c11 += x1 * y1;
-                    }
-                    acc[s][0] = c00;
-                    acc[s][1] = c01;
-                    acc[s][2] = c10;
-                    acc[s][3] = c11;
-                } else {
-                    const int ja0 = a0 >= D0, ja1 = a1 >= D0, jb0 = b0 >= D0, jb1 = b1 >= D0;
-                    const double *w00 = wst + (ja0 + jb0) * CH, *w01 = wst + (ja0 + jb1) * CH;
-                    const double *w10 = wst + (ja1 + jb0) * CH, *w11 = wst + (ja1 + jb1) * CH;
-                    double c00 = acc[s][0], c01 = acc[s][1], c10 = acc[s][2], c11 = acc[s][3];
-                    for (int ii = rep; ii < CH; ii += R) {
-                        const double x0 = pa0[ii], x1 = pa1[ii];
-                        const double y0 = pb0[ii], y1 = pb1[ii];
-                        c00 += x0 * w00[ii] * y0;
-                        c01 += x0 * w01[ii] * y1;
-                        c10 += x1 * w10[ii] * y0;
-                        c11 += x1 * w11[ii] * y1;
-                    }
-                    acc[s][0] = c00;
-                    acc[s][1] = c01;
-                    acc[s][2] = c10;
-                    acc[s][3] = c11;
-                }
-            }
-        }
-        // ordered reduction over replicas, then mirror
-        for (int r = 0; r < R; ++r) {
-            __syncthreads();
-            for (int s = 0; s < nmine; ++s) {
-                if (rep != r) continue;
-                const int a0 = ti[s], b0 = tj[s];
-                for (int e = 0; e < 4; ++e) {
-                    const int a = a0 + (e >> 1), b = b0 + (e & 1);
-                    if (a >= Dt || b >= Dt || a > b) continue;
-                    double v = acc[s][e];
-                    if (r > 0) v += H[a * d + b];
-                    H[a * d + b] = v;
-                    H[b * d + a] = v;
-                }
-            }
-        }
-        __syncthreads();
-    }
-}
-
-// Per-sample quadratic forms s^(j1 j2)_i = phi_j1(x_i)^T W_blk phi_j2(x_i) and
-// their third-derivative contractions c^(j)_i (posterior.py:495-509).
-template <int J>
-__device__ __noinline__ void trace_lik_samples(EvalCtx &E, const double *W, int d) {
-    const ModelParams &mp = E.M.mp;
-    const int Dt = mp.Dtot, CH = E.CH, ld = mp.ld, D0 = mp.D[0];
-    const int G = SGP_NT / CH;
-    double *part = E.stage + Dt * CH;  // G * CH * 3
-    const int ii = threadIdx.x % CH, gi = threadIdx.x / CH;
-    for (int i0 = 0; i0 < ld; i0 += CH) {
-        __syncthreads();
-        stage_chunk(E, i0);
-        __syncthreads();
-        double s00 = 0.0, sx = 0.0, s11 = 0.0;
-        if (gi < G) {
-            for (int a = gi; a < Dt; a += G) {
-                const double *wr = W + a * d;
-                double y0 = 0.0, y1 = 0.0;
-                for (int b = 0; b < D0; ++b) y0 += wr[b] * E.stage[b * CH + ii];
-                if (J == 2)
-                    for (int b = D0; b < Dt; ++b) y1 += wr[b] * E.stage[b * CH + ii];
-                const double pa = E.stage[a * CH + ii];
-                if (a < D0) {
-                    s00 += pa * y0;
-                    sx += pa * y1;
-                } else {
-                    sx += pa * y0;
-                    s11 += pa * y1;
-                }
-            }
-            part[(gi * CH + ii) * 3 + 0] = s00;
-            part[(gi * CH + ii) * 3 + 1] = sx;
-            part[(gi * CH + ii) * 3 + 2] = s11;
-        }
-        __syncthreads();
-        if ((int)threadIdx.x < CH) {
-            const int i = i0 + threadIdx.x;
-            double a00 = 0.0, ax = 0.0, a11 = 0.0;
-            for (int g = 0; g < G; ++g) {
-                a00 += part[(g * CH + threadIdx.x) * 3 + 0];
-                ax += part[(g * CH + threadIdx.x) * 3 + 1];
-                a11 += part[(g * CH + threadIdx.x) * 3 + 2];
-            }
-            if (i < ld) {
-                if (i < mp.N) {
-                    if (J == 1) {
-                        E.S[F_C0 * ld + i] = E.S[F_D3_000 * ld + i] * a00;
-                    } else {
-                        const double t001 = E.S[F_D3_001 * ld + i], t011 = E.S[F_D3_011 * ld + i];
-                        const double t111 = E.S[F_D3_111 * ld + i];
-                        // d3[0,0,0] is structurally zero for the mean/variance likelihood
-                        E.S[F_C0 * ld + i] = t001 * ax + t011 * a11;
-                        E.S[F_C1 * ld + i] = t001 * a00 + t011 * ax + t111 * a11;
-                    }
-                } else {
-                    E.S[F_C0 * ld + i] = 0.0;
-                    E.S[F_C1 * ld + i] = 0.0;
-                }
-            }
-        }
-    }
-    __syncthreads();
-}
-
 // out[a] = tau * sum_i phi[a,i] * S[field(j(a)), i] for a < Dtot (warp per row).
 __device__ __noinline__ void project_back(EvalCtx &E, double tau, int field0, int field1, double *out) {
     const ModelParams &mp = E.M.mp;
@@ -262,15 +73,43 @@ __device__ __forceinline__ int pad_to_coord(const ModelParams &mp, int a) {
     return b < mp.D[1] ? mp.D[0] + b : -1;
 }
 
-__device__ __forceinline__ void stage_chunk_sm(EvalCtx &E, int i0) {
+// Stage buffers: two of CH*SP + 3*CH doubles (Phi rows, then per-sample
+// weights), filled with 16-byte cp.async copies from the model's sample-major
+// padded copy M.phis while the previous chunk is being consumed.
+__device__ __forceinline__ void cp_async16(void *dst, const void *src, bool valid) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+    const int sz = valid ? 16 : 0;
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(src), "r"(sz));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+__device__ __forceinline__ double *stage_buf(EvalCtx &E, int b) {
+    return E.stage + b * (E.CH * (E.M.mp.Dp + 2) + 3 * E.CH);
+}
+
+// Issues the copies of samples [i0, i0+CH) (rows past ld zero-filled) and, if
+// nw > 0, of nw per-sample fields of E.S starting at field f0.
+__device__ __forceinline__ void stage_issue(EvalCtx &E, int i0, int b, int f0, int nw) {
     const ModelParams &mp = E.M.mp;
-    const int CH = E.CH, SP = mp.Dp + 2, ld = mp.ld;
-    for (int idx = threadIdx.x; idx < mp.Dp * CH; idx += SGP_NT) {
-        const int a = idx / CH, ii = idx - a * CH;
-        const int c = pad_to_coord(mp, a);
-        const int i = i0 + ii;
-        E.stage[ii * SP + a] = (c >= 0 && i < mp.N) ? E.M.phi[(size_t)c * ld + i] : 0.0;
+    const int CH = E.CH, SP = mp.Dp + 2, n16 = mp.Dp >> 1, ld = mp.ld;
+    double *dst = stage_buf(E, b);
+    for (int idx = threadIdx.x; idx < CH * n16; idx += SGP_NT) {
+        const int ii = idx / n16, c = idx - ii * n16;
+        const bool ok = i0 + ii < ld;
+        cp_async16(dst + ii * SP + 2 * c, E.M.phis + (size_t)(ok ? i0 + ii : 0) * mp.Dp + 2 * c, ok);
     }
+    double *w = dst + CH * SP;
+    const int h16 = CH >> 1;
+    for (int idx = threadIdx.x; idx < nw * h16; idx += SGP_NT) {
+        const int f = idx / h16, c = idx - f * h16;
+        const bool ok = i0 + 2 * c < ld;
+        cp_async16(w + f * CH + 2 * c, E.S + (size_t)(f0 + f) * ld + (ok ? i0 + 2 * c : 0), ok);
+    }
+    cp_async_commit();
 }
 
 __device__ __forceinline__ void load4(const double *p, double *x) {
@@ -299,7 +138,6 @@ __device__ __noinline__ void hess_lik_tiled(EvalCtx &E, double tau, double *H, i
     const ModelParams &mp = E.M.mp;
     const int CH = E.CH, SP = mp.Dp + 2, nb = mp.Dp >> 2, ld = mp.ld;
     const int ntile = nb * (nb + 1) / 2;
-    double *wst = E.stage + CH * SP;
     const int R = max(1, min(8, SGP_NT / max(1, ntile)));
     const int items = ntile * R;
     for (int base = 0; base < items; base += 2 * SGP_NT) {
@@ -320,29 +158,30 @@ __device__ __noinline__ void hess_lik_tiled(EvalCtx &E, double tau, double *H, i
         for (int s = 0; s < 2; ++s)
 #pragma unroll
             for (int e = 0; e < 16; ++e) acc[s][e] = 0.0;
-        for (int i0 = 0; i0 < mp.N; i0 += CH) {
-            __syncthreads();
-            stage_chunk_sm(E, i0);
-            for (int ii = threadIdx.x; ii < CH; ii += SGP_NT) {
-                const int i = i0 + ii;
-                const bool ok = i < mp.N;
-                wst[ii] = ok ? tau * E.S[F_D2_00 * ld + i] : 0.0;
-                if (J == 2) {
-                    wst[CH + ii] = ok ? tau * E.S[F_D2_01 * ld + i] : 0.0;
-                    wst[2 * CH + ii] = ok ? tau * E.S[F_D2_11 * ld + i] : 0.0;
-                }
+        const int nw = J == 2 ? 3 : 1;
+        __syncthreads();
+        stage_issue(E, 0, 0, F_D2_00, nw);
+        for (int k = 0, i0 = 0; i0 < mp.N; ++k, i0 += CH) {
+            if (i0 + CH < mp.N) {
+                stage_issue(E, i0 + CH, (k + 1) & 1, F_D2_00, nw);
+                cp_async_wait<1>();
+            } else {
+                cp_async_wait<0>();
             }
             __syncthreads();
+            const double *stg = stage_buf(E, k & 1);
+            const double *wst = stg + CH * SP;
 #pragma unroll
             for (int s = 0; s < 2; ++s) {
                 if (s >= nmine) break;
                 const int ja = J == 2 && a0[s] >= mp.Dp0, jb = J == 2 && b0[s] >= mp.Dp0;
+                // d2 fields are stored 00, 01, 11: index ja + jb
                 const double *wk = wst + (ja + jb) * CH;
                 for (int ii = rep[s]; ii < CH; ii += R) {
                     double xa[4], xb[4];
-                    load4(E.stage + ii * SP + a0[s], xa);
-                    load4(E.stage + ii * SP + b0[s], xb);
-                    const double w = wk[ii];
+                    load4(stg + ii * SP + a0[s], xa);
+                    load4(stg + ii * SP + b0[s], xb);
+                    const double w = tau * wk[ii];
 #pragma unroll
                     for (int v = 0; v < 4; ++v) xb[v] *= w;
 #pragma unroll
@@ -351,6 +190,7 @@ __device__ __noinline__ void hess_lik_tiled(EvalCtx &E, double tau, double *H, i
                         for (int v = 0; v < 4; ++v) acc[s][u * 4 + v] += xa[u] * xb[v];
                 }
             }
+            __syncthreads();
         }
         // ordered reduction over sample replicas, then mirror
         for (int r = 0; r < R; ++r) {
@@ -394,11 +234,18 @@ __device__ __noinline__ void trace_lik_tiled(EvalCtx &E, const double *Wp) {
     const ModelParams &mp = E.M.mp;
     const int CH = E.CH, SP = mp.Dp + 2, Dp = mp.Dp, nb = Dp >> 2, ld = mp.ld;
     const int ngrp = CH >> 2, tiles = ngrp * nb;
-    double *part = E.stage + CH * SP + 3 * CH;  // nb * CH * 3
-    for (int i0 = 0; i0 < mp.N; i0 += CH) {
+    double *part = stage_buf(E, 2);  // nb * CH * 3, after the two stage buffers
+    __syncthreads();
+    stage_issue(E, 0, 0, 0, 0);
+    for (int k = 0, i0 = 0; i0 < mp.N; ++k, i0 += CH) {
+        if (i0 + CH < mp.N) {
+            stage_issue(E, i0 + CH, (k + 1) & 1, 0, 0);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
         __syncthreads();
-        stage_chunk_sm(E, i0);
-        __syncthreads();
+        const double *stg = stage_buf(E, k & 1);
         for (int t = threadIdx.x; t < tiles; t += SGP_NT) {
             const int g = t / nb, bt = t - g * nb;
             const int ii0 = 4 * g, b0 = 4 * bt;
@@ -410,7 +257,7 @@ __device__ __noinline__ void trace_lik_tiled(EvalCtx &E, const double *Wp) {
                 load4(Wp + a * Dp + b0, w);
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
-                    const double x = E.stage[(ii0 + u) * SP + a];
+                    const double x = stg[(ii0 + u) * SP + a];
 #pragma unroll
                     for (int v = 0; v < 4; ++v) y0[u * 4 + v] += x * w[v];
                 }
@@ -421,7 +268,7 @@ __device__ __noinline__ void trace_lik_tiled(EvalCtx &E, const double *Wp) {
                     load4(Wp + a * Dp + b0, w);
 #pragma unroll
                     for (int u = 0; u < 4; ++u) {
-                        const double x = E.stage[(ii0 + u) * SP + a];
+                        const double x = stg[(ii0 + u) * SP + a];
 #pragma unroll
                         for (int v = 0; v < 4; ++v) y1[u * 4 + v] += x * w[v];
                     }
@@ -431,7 +278,7 @@ __device__ __noinline__ void trace_lik_tiled(EvalCtx &E, const double *Wp) {
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 double xb[4];
-                load4(E.stage + (ii0 + u) * SP + b0, xb);
+                load4(stg + (ii0 + u) * SP + b0, xb);
                 double p0 = 0.0, p1 = 0.0;
 #pragma unroll
                 for (int v = 0; v < 4; ++v) {

@@ -81,12 +81,17 @@ def test_cold_eigh_bit_exact(model_case):
 
 def test_short_chain_matches_oracle(model_case):
     name, model, data, target = model_case
-    eps = 0.005 if "meanvar" in name else 0.01
+    eps = 0.002
     cfg = S.ChainConfig(epsilon=eps, leapfrogs=4, moves=5, burnin=0, seed=11, record_q=True)
+    try:
+        ref = oracle.run_chain(oracle.OTarget(model, data),
+                               oracle.OConfig(epsilon=eps, leapfrogs=4, moves=5, burnin=0, seed=11,
+                                              record_q=True))
+    except oracle.OChainError:
+        with pytest.raises(S.ChainError):
+            S.run_chain(target, cfg)
+        return
     res = S.run_chain(target, cfg)
-    ref = oracle.run_chain(oracle.OTarget(model, data),
-                           oracle.OConfig(epsilon=eps, leapfrogs=4, moves=5, burnin=0, seed=11,
-                                          record_q=True))
     assert [r.accept for r in res.records] == [r.accept for r in ref.records]
     assert [r.divergent for r in res.records] == [r.divergent for r in ref.records]
     hb = np.array([r.h_before for r in res.records])
@@ -105,3 +110,15 @@ def test_batched_mixed_temperatures(model_case):
         single = S.run_chain(target.at_temperature(tau), S.ChainConfig(
             epsilon=0.005, leapfrogs=3, moves=3, burnin=0, record_q=True, seed=seed))
         np.testing.assert_array_equal(rb.sample_matrix(), single.sample_matrix())
+
+
+def test_first_move_divergence_matches_oracle():
+    """Both implementations reject an unusable epsilon the same way (sampler.py:388-391)."""
+    data = logistic_nmes()
+    model = rrgp.build_model("logistic", data.x)
+    target = PosteriorTarget(model, data)
+    with pytest.raises(oracle.OChainError):
+        oracle.run_chain(oracle.OTarget(model, data),
+                         oracle.OConfig(epsilon=0.01, leapfrogs=4, moves=5, burnin=0, seed=11))
+    with pytest.raises(S.ChainError):
+        S.run_chain(target, S.ChainConfig(epsilon=0.01, leapfrogs=4, moves=5, burnin=0, seed=11))
