@@ -8,9 +8,13 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <algorithm>
+#include <chrono>
+#include <cmath>
 #include <vector>
 
 #include "sgp_chain.cuh"
+#include "sgp_large.cuh"
 
 extern __shared__ __align__(16) char sgp_smem[];
 
@@ -18,7 +22,16 @@ struct sgp_model {
     ModelDev dev;
     double *d_phi, *d_phis, *d_y, *d_cw, *d_prec, *d_mean;
     int8_t *d_ckind;
+    // large-d path workspace (allocated on first use)
+    void *lg_owner;
+    LgPtrs lg;
 };
+
+static const LgPtrs *large_ws(const sgp_model *mc) {
+    sgp_model *m = const_cast<sgp_model *>(mc);
+    if (!m->lg_owner && lg_alloc(m->dev, m->lg, &m->lg_owner) != SGP_OK) return nullptr;
+    return &m->lg;
+}
 
 #define CUDA_TRY(x)                                                                  \
     do {                                                                             \
@@ -232,6 +245,7 @@ extern "C" int sgp_model_destroy(sgp_model *m) {
     if (!m) return SGP_OK;
     cudaFree(m->d_phi);
     cudaFree(m->d_phis);
+    if (m->lg_owner) cudaFree(m->lg_owner);
     cudaFree(m->d_y);
     cudaFree(m->d_cw);
     cudaFree(m->d_ckind);
@@ -248,7 +262,9 @@ extern "C" int sgp_model_features(const sgp_model *m, int j) {
     return m->dev.mp.D[j];
 }
 extern "C" size_t sgp_scratch_doubles(const sgp_model *m) {
-    return m ? sgp_scratch_per_chain(m->dev.mp.ld, m->dev.mp.d, m->dev.mp.Dp) : 0;
+    if (!m) return 0;
+    if (lg_is_large(m->dev)) return 64;  // the large path keeps its state in the model workspace
+    return sgp_scratch_per_chain(m->dev.mp.ld, m->dev.mp.d, m->dev.mp.Dp);
 }
 
 __global__ void k_phi_out(const double *phi, int ld, int N, int a0, int Dj, double *out) {
@@ -330,6 +346,11 @@ extern "C" int sgp_eval(const sgp_model *m, int Z, const double *d_tau, const do
     if (!m || Z < 1 || !d_tau || !d_q || !d_status || !d_scratch) return SGP_EINVAL;
     if ((what & SGP_EVAL_GRADIENT) && !d_grad) return SGP_EINVAL;
     if ((what & SGP_EVAL_HESSIAN) && !d_hess) return SGP_EINVAL;
+    if (lg_is_large(m->dev)) {
+        const LgPtrs *L = large_ws(m);
+        if (!L) return SGP_ENOMEM;
+        return lg_eval_api(*L, Z, d_tau, d_q, what & 15, d_pot, d_grad, d_hess, d_sumpot, d_status, S(stream));
+    }
     SmemPlan pl = plan_for(m, 0);
     int rc = launch_prep(k_eval, pl.bytes);
     if (rc) return rc;
@@ -363,6 +384,11 @@ __global__ void __launch_bounds__(SGP_MAX_NT) k_trace(ModelDev M, SmemPlan pl, c
 extern "C" int sgp_trace(const sgp_model *m, int Z, const double *d_tau, const double *d_q, const double *d_w,
                          double *d_t, int *d_status, double *d_scratch, void *stream) {
     if (!m || Z < 1 || !d_tau || !d_q || !d_w || !d_t || !d_status || !d_scratch) return SGP_EINVAL;
+    if (lg_is_large(m->dev)) {
+        const LgPtrs *L = large_ws(m);
+        if (!L) return SGP_ENOMEM;
+        return lg_trace_api(*L, Z, d_tau, d_q, d_w, d_t, d_status, S(stream));
+    }
     SmemPlan pl = plan_for(m, 0);
     int rc = launch_prep(k_trace, pl.bytes);
     if (rc) return rc;
@@ -638,6 +664,11 @@ extern "C" int sgp_leapfrog(const sgp_model *m, const sgp_chain_config *cfg, con
                             sgp_leapfrog_diag *diag, void *stream) {
     if (!m || !cfg || !st || !d_p || st->n_chains < 1) return SGP_EINVAL;
     if (cfg->fp_max_iters < 1 || cfg->fp_max_iters > 32) return SGP_EINVAL;
+    if (lg_is_large(m->dev)) {
+        const LgPtrs *L = large_ws(m);
+        if (!L) return SGP_ENOMEM;
+        return lg_leapfrog_api(*L, cfg, st, d_p, diag, S(stream));
+    }
     SmemPlan pl;
     chain_plan(m, pl);
     int rc = launch_prep(k_leapfrog, pl.bytes);
@@ -673,6 +704,11 @@ __global__ void __launch_bounds__(SGP_MAX_NT) k_chain_init(ModelDev M, SmemPlan 
 extern "C" int sgp_chain_init(const sgp_model *m, const sgp_chain_config *cfg, const sgp_chain_state *st,
                               void *stream) {
     if (!m || !cfg || !st || st->n_chains < 1) return SGP_EINVAL;
+    if (lg_is_large(m->dev)) {
+        const LgPtrs *L = large_ws(m);
+        if (!L) return SGP_ENOMEM;
+        return lg_chain_init(*L, cfg, st, S(stream));
+    }
     SmemPlan pl;
     chain_plan(m, pl);
     int rc = launch_prep(k_chain_init, pl.bytes);
@@ -789,6 +825,11 @@ extern "C" int sgp_run_moves(const sgp_model *m, const sgp_chain_config *cfg, co
         !rec->wall_ms)
         return SGP_EINVAL;
     if (moves == 0) return SGP_OK;
+    if (lg_is_large(m->dev)) {
+        const LgPtrs *LW = large_ws(m);
+        if (!LW) return SGP_ENOMEM;
+        return lg_run_moves(*LW, cfg, st, moves, move_offset, d_z, d_logu, rec, S(stream));
+    }
     const ChainLaunch L = chain_launch(m);
     const size_t spc = sgp_scratch_doubles(m);
     int rc;

@@ -89,6 +89,7 @@ __device__ inline void setup_ws(ChainWS &w, EvalCtx &E, char *smem, const SmemPl
     E.stage = reinterpret_cast<double *>(smem + pl.off_stage);
     E.CH = pl.CH;
     E.S = scratch;
+    E.ext_trace = 0;
     double **mats[SGP_NMAT] = {&w.H, &E.wp, &w.W, &w.P[0], &w.P[1], &w.X, &w.T};
     for (int i = 0; i < SGP_NMAT; ++i)
         *mats[i] = pl.off_mat[i] != (size_t)-1 ? reinterpret_cast<double *>(smem + pl.off_mat[i])

@@ -9,6 +9,8 @@ struct EvalCtx {
     double *S;      // per-sample fields, F_COUNT x ld (global scratch)
     double *stage;  // smem staging of a chunk of samples (see stage_chunk_sm)
     double *wp;     // padded Dp x Dp copy of the contraction matrix
+    int ext_trace;  // large-d path: 1 = c^(j) already in S; 2 = t[0, Dtot) already holds the likelihood part
+    double su_ext;  // large-d path: sum_i U_i computed by a grid reduction
     int CH;         // samples per chunk
     double *red;    // smem reduction scratch (>= 64 doubles)
     int *status;    // smem status word
@@ -322,6 +324,12 @@ __device__ __noinline__ void trace_lik_tiled(EvalCtx &E, const double *Wp) {
 
 // internal: per-sample fields in E.S already belong to q
 #define SGP_EVAL_REUSE 32
+// internal: with SGP_EVAL_HESSIAN, H already holds the likelihood block
+// (large-d path: DMMA GEMMs); only the prior terms are added
+#define SGP_EVAL_HPRIOR 64
+// internal (large-d path): per-sample fields, sum_i U_i (E.su_ext) and the
+// likelihood part of the gradient (grad[0, Dtot)) were produced by grid kernels
+#define SGP_EVAL_EXTLIK 128
 
 struct EvalOut {
     double pot, sumpot;
@@ -361,8 +369,12 @@ __device__ __noinline__ void eval_state(EvalCtx &E, const double *q, double tau,
 
     const bool need_lik = (tau != 0.0) || (what & SGP_EVAL_SUMPOT);
     const bool reuse = (what & SGP_EVAL_REUSE) != 0;  // S already holds this point
+    const bool extlik = (what & SGP_EVAL_EXTLIK) != 0;
     double su = 0.0;
-    if (need_lik && !reuse) {
+    if (extlik) {
+        su = E.su_ext;
+        o.sumpot = su;
+    } else if (need_lik && !reuse) {
         su = eval_lik(E, q);
         __syncthreads();
         if (*E.status) return;
@@ -372,7 +384,11 @@ __device__ __noinline__ void eval_state(EvalCtx &E, const double *q, double tau,
 
     // likelihood gradient and Hessian parts
     if (what & SGP_EVAL_GRADIENT) {
-        if (lik_on) {
+        if (extlik) {
+            if (!lik_on)
+                for (int a = threadIdx.x; a < mp.Dtot; a += SGP_NT) grad[a] = 0.0;
+            for (int a = mp.Dtot + threadIdx.x; a < d; a += SGP_NT) grad[a] = 0.0;
+        } else if (lik_on) {
             project_back(E, tau, F_D1_0, F_D1_1, grad);
             for (int a = mp.Dtot + threadIdx.x; a < d; a += SGP_NT) grad[a] = 0.0;
         } else {
@@ -380,7 +396,7 @@ __device__ __noinline__ void eval_state(EvalCtx &E, const double *q, double tau,
         }
         __syncthreads();
     }
-    if (what & SGP_EVAL_HESSIAN) {
+    if ((what & SGP_EVAL_HESSIAN) && !(what & SGP_EVAL_HPRIOR)) {
         for (int idx = threadIdx.x; idx < d * d; idx += SGP_NT) H[idx] = 0.0;
         __syncthreads();
         if (lik_on) {
@@ -494,12 +510,14 @@ __device__ __noinline__ void eval_trace(EvalCtx &E, const double *q, double tau,
         return;
     }
     if (tau != 0.0) {
-        build_wpad(mp, W, d, E.wp);
-        if (mp.J == 1)
-            trace_lik_tiled<1>(E, E.wp);
-        else
-            trace_lik_tiled<2>(E, E.wp);
-        project_back(E, tau, F_C0, F_C1, t);
+        if (!E.ext_trace) {
+            build_wpad(mp, W, d, E.wp);
+            if (mp.J == 1)
+                trace_lik_tiled<1>(E, E.wp);
+            else
+                trace_lik_tiled<2>(E, E.wp);
+        }
+        if (E.ext_trace != 2) project_back(E, tau, F_C0, F_C1, t);
         for (int a = mp.Dtot + threadIdx.x; a < d; a += SGP_NT) t[a] = 0.0;
     } else {
         for (int a = threadIdx.x; a < d; a += SGP_NT) t[a] = 0.0;

@@ -1,0 +1,241 @@
+// sgp_gemm.cuh — FP64 tensor-core (DMMA, mma.sync.m8n8k4.f64) GEMM for the
+// large-d path (d = 2083, N = 8192).
+//
+//   C[m][n] = alpha * sum_k A(m,k) * s(k) * B(k,n) + beta * C[m][n]
+//   A(m,k) = TA ? A[k*lda + m] : A[m*lda + k],  B(k,n) = TB ? B[n*ldb + k] : B[k*ldb + n]
+//   s(k) = scale ? scale[k] : 1   (diag(tau d2) of the likelihood Hessian)
+//
+// tcgen05 has no f64 kind; DMMA is the only FP64 tensor path on sm_100a and
+// measures 37.1 TF/s vs 34.3 TF/s for DFMA on B200 (profiles/r1_microbench.md).
+// CTA tile 64 x 64 x 32, 4 warps each owning a 32 x 32 sub-tile = 4 x 4 DMMA
+// fragments (32 accumulator doubles per thread).  Operand tiles keep their
+// global layout in shared memory so a 3-stage cp.async pipeline stages them
+// with 16-byte copies; row strides are padded by 4 doubles, which makes every
+// fragment load bank-conflict free.  Requires lda, ldb, ldc multiples of 2 and
+// 16-byte aligned bases (the large-path buffers are allocated that way).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define GM_BM 64
+#define GM_BN 64
+#define GM_BK 32
+#define GM_THREADS 128
+#define GM_STAGES 3
+
+struct GemmArgs {
+    int M, N, K;
+    const double *A;
+    int lda;
+    int TA;
+    const double *B;
+    int ldb;
+    int TB;
+    const double *scale;  // per-k multipliers or null
+    double *C;
+    int ldc;
+    double alpha, beta;
+    int upper_only;  // only tiles with m-tile <= n-tile (symmetric outputs, mirrored later)
+    int a16, b16;    // operand rows 16-byte aligned (set by gemm_launch); else 8-byte copies
+};
+
+__device__ __forceinline__ void dmma_m8n8k4(double &c0, double &c1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(c0), "+d"(c1)
+                 : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ void gm_cp16(void *dst, const void *src, bool valid) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(src), "r"(valid ? 16 : 0));
+}
+__device__ __forceinline__ void gm_cp8(void *dst, const void *src, bool valid) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(src), "r"(valid ? 8 : 0));
+}
+
+// shared tile geometry: "row" = the contiguous global dimension
+// A: TA ? [BK][BM] : [BM][BK];  B: TB ? [BN][BK] : [BK][BN]
+template <int TA, int TB>
+struct GmTile {
+    static constexpr int A_ROWS = TA ? GM_BK : GM_BM, A_COLS = TA ? GM_BM : GM_BK;
+    static constexpr int B_ROWS = TB ? GM_BN : GM_BK, B_COLS = TB ? GM_BK : GM_BN;
+    static constexpr int A_LD = A_COLS + 4, B_LD = B_COLS + 4;
+    static constexpr int A_SZ = A_ROWS * A_LD, B_SZ = B_ROWS * B_LD;
+    static constexpr int STAGE = A_SZ + B_SZ + GM_BK;  // + per-k scale
+    static constexpr size_t SMEM = (size_t)GM_STAGES * STAGE * sizeof(double);
+};
+
+template <int TA, int TB>
+__device__ __forceinline__ void gm_issue(const GemmArgs &g, double *st, int m0, int n0, int k0) {
+    using T = GmTile<TA, TB>;
+    const int tid = threadIdx.x;
+    double *As = st, *Bs = st + T::A_SZ, *Ss = st + T::A_SZ + T::B_SZ;
+    // A: rows of A_COLS doubles, A_COLS/2 16-byte chunks per row
+    constexpr int ACH = T::A_COLS / 2, BCH = T::B_COLS / 2;
+    if (!g.a16) {
+        for (int e = tid; e < T::A_ROWS * T::A_COLS; e += GM_THREADS) {
+            const int r = e / T::A_COLS, c = e - r * T::A_COLS;
+            const int gr = (TA ? k0 : m0) + r, gc = (TA ? m0 : k0) + c;
+            const bool ok = gr < (TA ? g.K : g.M) && gc < (TA ? g.M : g.K);
+            gm_cp8(As + r * T::A_LD + c, g.A + (ok ? (size_t)gr * g.lda + gc : 0), ok);
+        }
+    } else {
+#pragma unroll
+    for (int e = tid; e < T::A_ROWS * ACH; e += GM_THREADS) {
+        const int r = e / ACH, c = (e - r * ACH) * 2;
+        const int gr = (TA ? k0 : m0) + r, gc = (TA ? m0 : k0) + c;
+        const int rlim = TA ? g.K : g.M, clim = TA ? g.M : g.K;
+        const bool ok = gr < rlim && gc < clim;
+        // the pair (gc, gc+1): when gc+1 is past the edge the row tail is zero-filled by a 8-byte copy
+        const double *src = g.A + (size_t)(ok ? gr : 0) * g.lda + (ok ? gc : 0);
+        if (ok && gc + 1 >= clim) {
+            gm_cp8(As + r * T::A_LD + c, src, true);
+            gm_cp8(As + r * T::A_LD + c + 1, src, false);
+        } else {
+            gm_cp16(As + r * T::A_LD + c, src, ok);
+        }
+    }
+    }
+    if (!g.b16) {
+        for (int e = tid; e < T::B_ROWS * T::B_COLS; e += GM_THREADS) {
+            const int r = e / T::B_COLS, c = e - r * T::B_COLS;
+            const int gr = (TB ? n0 : k0) + r, gc = (TB ? k0 : n0) + c;
+            const bool ok = gr < (TB ? g.N : g.K) && gc < (TB ? g.K : g.N);
+            gm_cp8(Bs + r * T::B_LD + c, g.B + (ok ? (size_t)gr * g.ldb + gc : 0), ok);
+        }
+    } else
+#pragma unroll
+    for (int e = tid; e < T::B_ROWS * BCH; e += GM_THREADS) {
+        const int r = e / BCH, c = (e - r * BCH) * 2;
+        const int gr = (TB ? n0 : k0) + r, gc = (TB ? k0 : n0) + c;
+        const int rlim = TB ? g.N : g.K, clim = TB ? g.K : g.N;
+        const bool ok = gr < rlim && gc < clim;
+        const double *src = g.B + (size_t)(ok ? gr : 0) * g.ldb + (ok ? gc : 0);
+        if (ok && gc + 1 >= clim) {
+            gm_cp8(Bs + r * T::B_LD + c, src, true);
+            gm_cp8(Bs + r * T::B_LD + c + 1, src, false);
+        } else {
+            gm_cp16(Bs + r * T::B_LD + c, src, ok);
+        }
+    }
+    if (g.scale && tid < GM_BK / 2) {
+        const int c = tid * 2;
+        const bool ok = k0 + c < g.K;
+        if (ok && k0 + c + 1 >= g.K) {
+            gm_cp8(Ss + c, g.scale + k0 + c, true);
+            gm_cp8(Ss + c + 1, g.scale, false);
+        } else {
+            gm_cp16(Ss + c, g.scale + (ok ? k0 + c : 0), ok);
+        }
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+}
+
+template <int TA, int TB>
+__global__ void __launch_bounds__(GM_THREADS) k_gemm_dmma(GemmArgs g) {
+    using T = GmTile<TA, TB>;
+    const int tm = blockIdx.y, tn = blockIdx.x;
+    if (g.upper_only && tm > tn) return;
+    extern __shared__ __align__(16) double gsm[];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+    const int gid = lane >> 2, tig = lane & 3;
+    const int m0 = tm * GM_BM, n0 = tn * GM_BN;
+    const bool has_scale = g.scale != nullptr;
+    double acc[4][4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    const int nk = (g.K + GM_BK - 1) / GM_BK;
+#pragma unroll
+    for (int s = 0; s < GM_STAGES - 1; ++s) {
+        if (s < nk)
+            gm_issue<TA, TB>(g, gsm + s * T::STAGE, m0, n0, s * GM_BK);
+        else
+            asm volatile("cp.async.commit_group;\n" ::);
+    }
+    for (int kt = 0; kt < nk; ++kt) {
+        asm volatile("cp.async.wait_group %0;\n" ::"n"(GM_STAGES - 2));
+        __syncthreads();
+        const int nxt = kt + GM_STAGES - 1;
+        if (nxt < nk)
+            gm_issue<TA, TB>(g, gsm + (nxt % GM_STAGES) * T::STAGE, m0, n0, nxt * GM_BK);
+        else
+            asm volatile("cp.async.commit_group;\n" ::);
+        const double *As = gsm + (kt % GM_STAGES) * T::STAGE;
+        const double *Bs = As + T::A_SZ, *Ss = As + T::A_SZ + T::B_SZ;
+#pragma unroll
+        for (int k4 = 0; k4 < GM_BK; k4 += 4) {
+            const int kk = k4 + tig;
+            double af[4], bf[4];
+            const double sk = has_scale ? Ss[kk] : 1.0;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int mm = wm + i * 8 + gid;
+                af[i] = (TA ? As[kk * T::A_LD + mm] : As[mm * T::A_LD + kk]) * sk;
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int nn = wn + j * 8 + gid;
+                bf[j] = TB ? Bs[nn * T::B_LD + kk] : Bs[kk * T::B_LD + nn];
+            }
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) dmma_m8n8k4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+        }
+    }
+    asm volatile("cp.async.wait_group 0;\n" ::);
+    // epilogue: C fragment (row gid, cols 2*tig, 2*tig+1)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int m = m0 + wm + i * 8 + gid;
+        if (m >= g.M) continue;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int n = n0 + wn + j * 8 + 2 * tig + h;
+                if (n >= g.N) continue;
+                double v = g.alpha * acc[i][j][h];
+                double *cp = g.C + (size_t)m * g.ldc + n;
+                if (g.beta != 0.0) v += g.beta * *cp;
+                *cp = v;
+            }
+        }
+    }
+}
+
+// mirror the upper triangle of an n x n matrix into the lower one
+__global__ void k_mirror_upper(double *C, int n, int ldc) {
+    for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < (size_t)n * n;
+         idx += (size_t)gridDim.x * blockDim.x) {
+        const int i = (int)(idx / n), j = (int)(idx - (size_t)i * n);
+        if (i > j) C[(size_t)i * ldc + j] = C[(size_t)j * ldc + i];
+    }
+}
+
+template <int TA, int TB>
+static inline cudaError_t gemm_launch_t(const GemmArgs &g, cudaStream_t s) {
+    using T = GmTile<TA, TB>;
+    static bool configured = false;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(k_gemm_dmma<TA, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)T::SMEM);
+        if (e != cudaSuccess) return e;
+        configured = true;
+    }
+    dim3 grid((g.N + GM_BN - 1) / GM_BN, (g.M + GM_BM - 1) / GM_BM);
+    k_gemm_dmma<TA, TB><<<grid, GM_THREADS, T::SMEM, s>>>(g);
+    return cudaGetLastError();
+}
+
+static inline cudaError_t gemm_launch(GemmArgs g, cudaStream_t s) {
+    g.a16 = (g.lda % 2 == 0) && ((reinterpret_cast<uintptr_t>(g.A) & 15) == 0);
+    g.b16 = (g.ldb % 2 == 0) && ((reinterpret_cast<uintptr_t>(g.B) & 15) == 0);
+    if (g.TA)
+        return g.TB ? gemm_launch_t<1, 1>(g, s) : gemm_launch_t<1, 0>(g, s);
+    return g.TB ? gemm_launch_t<0, 1>(g, s) : gemm_launch_t<0, 0>(g, s);
+}

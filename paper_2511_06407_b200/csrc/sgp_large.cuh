@@ -1,0 +1,1087 @@
+// sgp_large.cuh — large-d path (nl-meanvar, N = 8192,
+// d = 2083), one chain at a time occupying the whole GPU.
+//
+// The O(N d^2) and O(d^3) contractions run as DMMA GEMMs (sgp_gemm.cuh):
+//   Hessian   H_lik[j1,j2] = Phi_j1^T diag(tau d2_{j1 j2}) Phi_j2      (posterior.py:449-460)
+//   trace     Y_j1 = Phi_j1 W[blk j1, :], s^(j1 j2)_i = <Y_j1[i, blk j2], phi_j2(x_i)>   (:495-509)
+//   metric    W = Psi M Psi^T, M = diag((lam/g)/g) - (b b^T) o T       (metric.py:188-204)
+//   warm eigh A = Psi^T H Psi                                           (metric.py:170)
+// The warm Jacobi uses the round-robin parallel order grid-wide (d/2
+// rotations per round, rows then columns), with the reference's skip rule
+// and convergence test; cold decompositions keep the reference order
+// (bit-exact, one warp; only at chain start and rejections).  The O(d) and
+// O(N d) glue (per-sample derivatives, prior terms, mat-vecs, fixed-point
+// updates) reuses the CTA-level functions on one CTA.  The leapfrog control
+// flow runs on the host thread, reading back one status/delta word per
+// fixed-point iteration.
+#pragma once
+#include "sgp_chain.cuh"
+#include "sgp_gemm.cuh"
+
+#define LG_NT 256
+
+struct LgPtrs {
+    ModelDev M;
+    double *S, *H, *X, *W, *P[2], *Y, *sacc, *vec, *sc, *jlog, *jprm, *red;
+    int *si, *status, *jpairs;
+};
+
+struct LargeWS {
+    LgPtrs p;
+    size_t bytes;
+};
+
+__device__ inline void lg_setup(ChainWS &w, EvalCtx &E, const LgPtrs &L, char *smem) {
+    const int d = L.M.mp.d;
+    E.M = L.M;
+    E.red = reinterpret_cast<double *>(smem);
+    E.status = L.status;
+    E.S = L.S;
+    E.stage = nullptr;
+    E.wp = nullptr;
+    E.CH = 32;
+    E.ext_trace = 2;
+    E.su_ext = 0.0;
+    w.sc = L.sc;
+    w.si = L.si;
+    double **vecs[] = {&w.q0, &w.qc, &w.qn, &w.qs, &w.p, &w.ph, &w.pn, &w.v0, &w.grad, &w.tv, &w.bv, &w.tmp,
+                       &w.lam[0], &w.lam[1], &w.g[0], &w.g[1]};
+    for (int k = 0; k < 16; ++k) *vecs[k] = L.vec + (size_t)k * d;
+    w.H = L.H;
+    w.X = L.X;
+    w.W = L.W;
+    w.P[0] = L.P[0];
+    w.P[1] = L.P[1];
+    w.T = nullptr;
+    w.prm = L.jprm;
+    w.jlog = L.jlog;
+}
+
+// single-CTA glue operations
+enum LgOp {
+    LG_STATE = 0,      // eval_state(q = vec[a0], what = i0): pot -> sc[2], sumpot -> sc[3]
+    LG_TRACE = 1,      // t -> tv from S (c^(j) precomputed) at q = vec[a0]
+    LG_BVEC = 2,       // bv = Psi_slot^T p(vec[a0]) / g_slot
+    LG_APPLY = 3,      // vec[a1] = metric_apply(P_slot, g_slot, vec[a0], mode i0)
+    LG_GLAM = 4,       // lam_slot = diag(H); g_slot, logdet -> sc[slot]; since -> si[slot] = i0
+    LG_MGS = 5,        // mgs(P_slot)
+    LG_KINETIC = 6,    // sc[6] = kinetic(p, slot)
+    LG_COLD = 7,       // cold cyclic Jacobi of H into P_slot (bit-exact reference order)
+    LG_OFFNORM = 8,    // sc[7] = off-norm of H (full storage)
+    LG_LOADFRAME = 9,  // P_0 <- psi, lam_0 <- lam (from chain state), since
+    LG_QDELTA = 10,    // qn = q0 + 0.5 eps (v0 + tmp); sc[5] = max|qn - qc|
+    LG_PHALF = 11,     // out = p - 0.5 eps (grad + 0.5 tv); sc[5] = max|out - ph| if i0
+    LG_JCYC = 12,      // reference-order Jacobi of H (as is) into P_slot (as is), tol sc[9], skip sc[10]
+};
+
+struct LgOpArgs {
+    int op, slot, a0, a1, i0;
+    double eps;
+    sgp_chain_config cfg;
+    double tau;
+};
+
+__global__ void __launch_bounds__(LG_NT) k_lg_op(LgPtrs L, LgOpArgs a) {
+    __shared__ __align__(16) char smem[128 * sizeof(double)];
+    ChainWS w;
+    EvalCtx E;
+    lg_setup(w, E, L, smem);
+    const int d = L.M.mp.d;
+    double *V = L.vec;
+    switch (a.op) {
+        case LG_STATE: {
+            EvalOut o;
+            E.su_ext = w.sc[3];
+            eval_state(E, V + (size_t)a.a0 * d, a.tau, a.i0 | SGP_EVAL_EXTLIK, w.grad, w.H, o);
+            // a gradient-only pass over an already evaluated point keeps the stored potential
+            if (threadIdx.x == 0 && !(a.i0 & SGP_EVAL_REUSE)) w.sc[2] = o.pot;
+            break;
+        }
+        case LG_TRACE:
+            eval_trace(E, V + (size_t)a.a0 * d, a.tau, w.W, w.tv);
+            break;
+        case LG_BVEC:
+            mat_tvec(w.bv, w.P[a.slot], V + (size_t)a.a0 * d, d);
+            for (int j = threadIdx.x; j < d; j += SGP_NT) w.bv[j] /= w.g[a.slot][j];
+            break;
+        case LG_APPLY:
+            metric_apply(V + (size_t)a.a1 * d, w.bv, w.P[a.slot], w.g[a.slot], V + (size_t)a.a0 * d, d, a.i0);
+            break;
+        case LG_GLAM: {
+            for (int j = threadIdx.x; j < d; j += SGP_NT) w.lam[a.slot][j] = w.H[(size_t)j * d + j];
+            __syncthreads();
+            const double ld = metric_g(w.lam[a.slot], w.g[a.slot], d, a.cfg.kappa, E.red);
+            if (threadIdx.x == 0) {
+                w.sc[a.slot] = ld;
+                w.si[a.slot] = a.i0;
+            }
+            break;
+        }
+        case LG_MGS:
+            mgs(w.P[a.slot], d, E.red);
+            break;
+        case LG_KINETIC: {
+            const double qd = metric_quad(w.tmp, w.P[a.slot], w.g[a.slot], w.p, d, E.red);
+            if (threadIdx.x == 0) w.sc[6] = 0.5 * qd + 0.5 * (d * SGP_LN_2PI + w.sc[a.slot]);
+            break;
+        }
+        case LG_COLD: {
+            mat_symmetrize(w.H, d);
+            const double hnorm = sqrt(frob2(w.H, d * d, E.red));
+            const double tol = a.cfg.zeta * hnorm;
+            const double skip = d ? tol / d : 0.0;
+            mat_identity(w.P[a.slot], d);
+            const int sw = jacobi_cyclic(w.H, w.P[a.slot], d, tol, skip, a.cfg.sweep_cap, E.red, w.jlog);
+            if (threadIdx.x == 0) {
+                w.si[4] = sw;
+                if (sw < 0) *E.status = SGP_STATUS_JACOBI;
+            }
+            break;
+        }
+        case LG_JCYC: {
+            const int sw = jacobi_cyclic(w.H, w.P[a.slot], d, w.sc[9], w.sc[10], a.cfg.sweep_cap, E.red, w.jlog);
+            if (threadIdx.x == 0) {
+                w.si[4] = sw;
+                if (sw < 0) *E.status = SGP_STATUS_JACOBI;
+            }
+            break;
+        }
+        case LG_OFFNORM: {
+            const double off = sqrt(offdiag2(w.H, d, E.red));
+            if (threadIdx.x == 0) w.sc[7] = off;
+            break;
+        }
+        case LG_QDELTA: {
+            double dl = 0.0;
+            bool nan_here = false;
+            for (int j = threadIdx.x; j < d; j += SGP_NT) {
+                const double qn = w.q0[j] + 0.5 * a.eps * (w.v0[j] + w.tmp[j]);
+                w.qn[j] = qn;
+                dl = fmax(dl, fabs(qn - w.qc[j]));
+                nan_here |= isnan(qn - w.qc[j]);
+            }
+            const double delta = block_max_nan(nan_here ? NAN : dl, E.red);
+            if (threadIdx.x == 0) w.sc[5] = delta;
+            break;
+        }
+        case LG_PHALF: {
+            // out = vec[a1]; p = w.p; grad, tv
+            double *out = V + (size_t)a.a1 * d;
+            double dl = 0.0;
+            bool nan_here = false;
+            for (int j = threadIdx.x; j < d; j += SGP_NT) {
+                const double v = w.p[j] - 0.5 * a.eps * (w.grad[j] + 0.5 * w.tv[j]);
+                if (a.i0) {
+                    dl = fmax(dl, fabs(v - w.ph[j]));
+                    nan_here |= isnan(v - w.ph[j]);
+                }
+                out[j] = v;
+            }
+            if (a.i0) {
+                const double delta = block_max_nan(nan_here ? NAN : dl, E.red);
+                if (threadIdx.x == 0) w.sc[5] = delta;
+            }
+            break;
+        }
+        default:
+            break;
+    }
+}
+
+// M[j][l] = [(lam/g)/g]_j delta_jl + c1 b_j T_jl b_l, T from lam, g (metric.py:46-59)
+__global__ void k_lg_mmat(LgPtrs L, int slot, double kappa, double c1, int with_w1, int with_w2) {
+    const int d = L.M.mp.d;
+    const double *lam = L.vec + (size_t)(12 + slot) * d, *g = L.vec + (size_t)(14 + slot) * d;
+    const double *b = L.vec + (size_t)10 * d;
+    for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < (size_t)d * d;
+         idx += (size_t)gridDim.x * blockDim.x) {
+        const int j = (int)(idx / d), l = (int)(idx - (size_t)j * d);
+        double m = 0.0;
+        if (with_w1) {
+            const double diff = lam[j] - lam[l];
+            const double T = (fabs(diff) <= kappa * 1e-10) ? lam[j] / g[j] : (g[j] - g[l]) / diff;
+            m = c1 * ((b[j] * T) * b[l]);
+        }
+        if (with_w2 && j == l) m += (lam[j] / g[j]) / g[j];
+        L.W[idx] = m;
+    }
+}
+
+__global__ void k_lg_symmetrize(double *A, int d) {
+    for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < (size_t)d * d;
+         idx += (size_t)gridDim.x * blockDim.x) {
+        const int i = (int)(idx / d), j = (int)(idx - (size_t)i * d);
+        if (i < j) {
+            const double v = 0.5 * (A[idx] + A[(size_t)j * d + i]);
+            A[idx] = v;
+            A[(size_t)j * d + i] = v;
+        }
+    }
+}
+
+__global__ void k_lg_copy(double *dst, const double *src, size_t n) {
+    for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < n; idx += (size_t)gridDim.x * blockDim.x)
+        dst[idx] = src[idx];
+}
+
+__global__ void k_lg_zero(double *dst, size_t n) {
+    for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < n; idx += (size_t)gridDim.x * blockDim.x)
+        dst[idx] = 0.0;
+}
+
+// per-sample quadratic forms from Y_j1 (ld x Dtot, coordinate columns): warp per sample
+__global__ void k_lg_rowdot(LgPtrs L, int j1, int final_pass) {
+    const ModelParams &mp = L.M.mp;
+    const int Dt = mp.Dtot, ld = mp.ld;
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    const int nw = (gridDim.x * blockDim.x) >> 5;
+    for (int i = warp; i < mp.N; i += nw) {
+        const double *y = L.Y + (size_t)i * Dt;
+        const double *ph = L.M.phis + (size_t)i * mp.Dp;
+        double s0 = 0.0, s1 = 0.0;
+        for (int b = lane; b < Dt; b += 32) {
+            const bool blk1 = b >= mp.D[0];
+            const int pb = blk1 ? mp.Dp0 + (b - mp.D[0]) : b;
+            const double v = y[b] * ph[pb];
+            if (blk1)
+                s1 += v;
+            else
+                s0 += v;
+        }
+        s0 = warp_sum(s0);
+        s1 = warp_sum(s1);
+        if (lane == 0) {
+            double *sa = L.sacc;
+            if (j1 == 0) {
+                sa[i] = s0;           // s00
+                sa[ld + i] = s1;      // s01 (cross, first half)
+                sa[2 * ld + i] = 0.0;
+            } else {
+                sa[ld + i] += s0;     // s10
+                sa[2 * ld + i] = s1;  // s11
+            }
+            if (final_pass) {
+                double *S = L.S;
+                if (mp.J == 1) {
+                    S[F_C0 * ld + i] = S[F_D3_000 * ld + i] * sa[i];
+                } else {
+                    const double a00 = sa[i], ax = sa[ld + i], a11 = sa[2 * ld + i];
+                    const double t001 = S[F_D3_001 * ld + i], t011 = S[F_D3_011 * ld + i];
+                    const double t111 = S[F_D3_111 * ld + i];
+                    S[F_C0 * ld + i] = t001 * ax + t011 * a11;
+                    S[F_C1 * ld + i] = t001 * a00 + t011 * ax + t111 * a11;
+                }
+            }
+        }
+    }
+}
+
+// ---- grid-parallel Jacobi (round-robin order) -------------------------------
+// prm per pair: c, s, t*apq, app, aqq ; pairs: p, q (p = -1 inactive)
+__global__ void k_lg_jrows(double *A, int d, int r, double skip, double *prm, int *pairs) {
+    const int m = d + (d & 1), np = m >> 1;
+    const int k = blockIdx.x;
+    if (k >= np) return;
+    __shared__ double cs[2];
+    __shared__ int pq[2];
+    if (threadIdx.x == 0) {
+        int a, b;
+        if (k == 0) {
+            a = r;
+            b = m - 1;
+        } else {
+            a = (r + k) % (m - 1);
+            b = (r - k + m - 1) % (m - 1);
+        }
+        int p = min(a, b), q = max(a, b);
+        int act = 0;
+        if (q < d) {
+            const double apq = A[(size_t)p * d + q];
+            if (fabs(apq) > skip) {
+                const double app = A[(size_t)p * d + p], aqq = A[(size_t)q * d + q];
+                double c, s, t;
+                jacobi_rot(app, aqq, apq, c, s, t);
+                prm[5 * k + 0] = c;
+                prm[5 * k + 1] = s;
+                prm[5 * k + 2] = t * apq;
+                prm[5 * k + 3] = app;
+                prm[5 * k + 4] = aqq;
+                cs[0] = c;
+                cs[1] = s;
+                act = 1;
+            }
+        }
+        pq[0] = act ? p : -1;
+        pq[1] = q;
+        pairs[2 * k] = pq[0];
+        pairs[2 * k + 1] = q;
+    }
+    __syncthreads();
+    const int p = pq[0];
+    if (p < 0) return;
+    const int q = pq[1];
+    const double c = cs[0], s = cs[1];
+    double *rp = A + (size_t)p * d, *rq = A + (size_t)q * d;
+    for (int l = threadIdx.x; l < d; l += blockDim.x) {
+        const double ap = rp[l], aq = rq[l];
+        rp[l] = c * ap - s * aq;
+        rq[l] = s * ap + c * aq;
+    }
+}
+
+__global__ void k_lg_jcols(double *A, double *V, int d, const double *prm, const int *pairs) {
+    const int m = d + (d & 1), np = m >> 1;
+    // one CTA per row l; threads over pairs
+    for (int l = blockIdx.x; l < d; l += gridDim.x) {
+        double *ra = A + (size_t)l * d, *rv = V + (size_t)l * d;
+        for (int k = threadIdx.x; k < np; k += blockDim.x) {
+            const int p = pairs[2 * k];
+            if (p < 0) continue;
+            const int q = pairs[2 * k + 1];
+            const double c = prm[5 * k], s = prm[5 * k + 1];
+            const double ap = ra[p], aq = ra[q];
+            ra[p] = c * ap - s * aq;
+            ra[q] = s * ap + c * aq;
+            const double vp = rv[p], vq = rv[q];
+            rv[p] = c * vp - s * vq;
+            rv[q] = s * vp + c * vq;
+            if (l == p) {
+                ra[p] = prm[5 * k + 3] - prm[5 * k + 2];
+                ra[q] = 0.0;
+            } else if (l == q) {
+                ra[q] = prm[5 * k + 4] + prm[5 * k + 2];
+                ra[p] = 0.0;
+            }
+        }
+    }
+}
+
+__global__ void k_lg_transpose_block(double *H, int d, int r0, int c0, int nr, int nc) {
+    // H[c0 + j][r0 + i] = H[r0 + i][c0 + j]
+    for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < (size_t)nr * nc;
+         idx += (size_t)gridDim.x * blockDim.x) {
+        const int i = (int)(idx / nc), j = (int)(idx - (size_t)i * nc);
+        H[(size_t)(c0 + j) * d + r0 + i] = H[(size_t)(r0 + i) * d + c0 + j];
+    }
+}
+
+__global__ void k_lg_mirror_block(double *H, int d, int o, int n) {
+    for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < (size_t)n * n;
+         idx += (size_t)gridDim.x * blockDim.x) {
+        const int i = (int)(idx / n), j = (int)(idx - (size_t)i * n);
+        if (i > j) H[(size_t)(o + i) * d + o + j] = H[(size_t)(o + j) * d + o + i];
+    }
+}
+
+__global__ void k_lg_frob(const double *A, size_t n, double *out) {
+    __shared__ double red[64];
+    double s = 0.0;
+    for (size_t idx = threadIdx.x; idx < n; idx += blockDim.x) s += A[idx] * A[idx];
+    s = block_sum(s, red);
+    if (threadIdx.x == 0) *out = s;
+}
+
+__global__ void k_lg_eye(double *P, int d) {
+    for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < (size_t)d * d;
+         idx += (size_t)gridDim.x * blockDim.x)
+        P[idx] = (idx / d == idx % d) ? 1.0 : 0.0;
+}
+
+__global__ void k_lg_set2(double *dst, double a, double b) {
+    dst[0] = a;
+    dst[1] = b;
+}
+
+// ---- grid-wide O(N d) glue ------------------------------------------------
+// latent values and per-sample derivatives; block partial sums of U and a
+// non-finite flag into red[blockIdx.x], red[gridDim.x + blockIdx.x]
+__global__ void __launch_bounds__(256) k_lg_lik(LgPtrs L, const double *q) {
+    __shared__ double red[64];
+    const ModelParams &mp = L.M.mp;
+    const int ld = mp.ld;
+    double su = 0.0, bad = 0.0;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < ld; i += gridDim.x * blockDim.x) {
+        double f0 = 0.0, f1 = 0.0;
+        for (int a = 0; a < mp.D[0]; ++a) f0 += L.M.phi[(size_t)a * ld + i] * q[a];
+        if (mp.J == 2)
+            for (int a = 0; a < mp.D[1]; ++a) f1 += L.M.phi[(size_t)(mp.D[0] + a) * ld + i] * q[mp.fstart[1] + a];
+        if (i < mp.N) {
+            if (!isfinite(f0) || !isfinite(f1)) bad = 1.0;
+            L.S[F_F0 * ld + i] = f0;
+            L.S[F_F1 * ld + i] = f1;
+            lik_sample(mp.lik, mp.vfloor, L.M.y[i], f0, f1, L.S, ld, i);
+            su += L.S[F_U * ld + i];
+        } else {
+            for (int k = 0; k < F_COUNT; ++k) L.S[k * ld + i] = 0.0;
+        }
+    }
+    su = block_sum(su, red);
+    __syncthreads();
+    bad = block_sum(bad, red);
+    if (threadIdx.x == 0) {
+        L.red[blockIdx.x] = su;
+        L.red[gridDim.x + blockIdx.x] = bad;
+    }
+}
+
+// sc[3] = sum of the block partials (fixed order); status DIVERGENCE on a flag
+__global__ void k_lg_lik_finish(LgPtrs L, int nblocks) {
+    if (threadIdx.x != 0) return;
+    double su = 0.0, bad = 0.0;
+    for (int b = 0; b < nblocks; ++b) {
+        su += L.red[b];
+        bad += L.red[nblocks + b];
+    }
+    L.sc[3] = su;
+    if (bad > 0.0 && *L.status == 0) *L.status = SGP_STATUS_DIVERGENCE;
+}
+
+// out[a] = tau sum_i phi[a, i] S[field(j(a)), i] for a < Dtot (warp per row)
+__global__ void k_lg_project(LgPtrs L, double tau, int field0, int field1, double *out) {
+    const ModelParams &mp = L.M.mp;
+    const int ld = mp.ld;
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    const int nw = (gridDim.x * blockDim.x) >> 5;
+    for (int a = warp; a < mp.Dtot; a += nw) {
+        const int f = (a < mp.D[0]) ? field0 : field1;
+        const double *pr = L.M.phi + (size_t)a * ld;
+        const double *sr = L.S + (size_t)f * ld;
+        double s = 0.0;
+        for (int i = lane; i < mp.N; i += 32) s += pr[i] * sr[i];
+        s = warp_sum(s);
+        if (lane == 0) out[a] = tau * s;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// host driver
+
+enum { V_Q0 = 0, V_QC, V_QN, V_QS, V_P, V_PH, V_PN, V_V0, V_GRAD, V_TV, V_BV, V_TMP, V_LAM0, V_LAM1, V_G0, V_G1 };
+
+static inline int lg_blocks(size_t n) { return (int)std::min<size_t>((n + 255) / 256, 148 * 16); }
+
+struct LgCtx {
+    LgPtrs L;
+    cudaStream_t s;
+    sgp_chain_config cfg;
+    double tau;
+    int d;
+    double sc[16];  // host mirrors of the device scalars
+    int si[16];
+    int status;
+    int since[2];
+};
+
+static void lg_op(LgCtx &c, int op, int slot = 0, int a0 = 0, int a1 = 0, int i0 = 0, double eps = 0.0) {
+    LgOpArgs a;
+    a.op = op;
+    a.slot = slot;
+    a.a0 = a0;
+    a.a1 = a1;
+    a.i0 = i0;
+    a.eps = eps;
+    a.cfg = c.cfg;
+    a.tau = c.tau;
+    k_lg_op<<<1, LG_NT, 0, c.s>>>(c.L, a);
+}
+
+static int lg_sync(LgCtx &c) {
+    cudaMemcpyAsync(c.sc, c.L.sc, sizeof(c.sc), cudaMemcpyDeviceToHost, c.s);
+    cudaMemcpyAsync(c.si, c.L.si, sizeof(c.si), cudaMemcpyDeviceToHost, c.s);
+    cudaMemcpyAsync(&c.status, c.L.status, sizeof(int), cudaMemcpyDeviceToHost, c.s);
+    if (cudaStreamSynchronize(c.s) != cudaSuccess) return -1;
+    return c.status;
+}
+
+static void lg_clear_status(LgCtx &c) { cudaMemsetAsync(c.L.status, 0, sizeof(int), c.s); }
+
+static void lg_gemm(LgCtx &c, int M, int N, int K, const double *A, int lda, int TA, const double *B, int ldb, int TB,
+                    const double *scale, double *C, int ldc, double alpha, int upper) {
+    GemmArgs g{};
+    g.M = M;
+    g.N = N;
+    g.K = K;
+    g.A = A;
+    g.lda = lda;
+    g.TA = TA;
+    g.B = B;
+    g.ldb = ldb;
+    g.TB = TB;
+    g.scale = scale;
+    g.C = C;
+    g.ldc = ldc;
+    g.alpha = alpha;
+    g.beta = 0.0;
+    g.upper_only = upper;
+    gemm_launch(g, c.s);
+}
+
+// State at vec[qv]: potential (sc[2]), sum U (sc[3]), gradient (vec GRAD) if
+// asked, per-sample fields; Hessian into H via DMMA GEMMs + prior terms.
+static int lg_state(LgCtx &c, int qv, int what) {
+    const ModelParams &mp = c.L.M.mp;
+    const int d = c.d;
+    const bool hess = what & SGP_EVAL_HESSIAN;
+    const bool lik = mp.lik != SGP_LIK_QUADRATIC && (c.tau != 0.0 || (what & SGP_EVAL_SUMPOT));
+    if (lik && !(what & SGP_EVAL_REUSE)) {
+        const int nb = 148;
+        k_lg_lik<<<nb, 256, 0, c.s>>>(c.L, c.L.vec + (size_t)qv * d);
+        k_lg_lik_finish<<<1, 32, 0, c.s>>>(c.L, nb);
+    } else if (!(what & SGP_EVAL_REUSE)) {
+        k_lg_set2<<<1, 1, 0, c.s>>>(c.L.sc + 3, 0.0, c.sc[4]);
+    }
+    if ((what & SGP_EVAL_GRADIENT) && c.tau != 0.0 && mp.lik != SGP_LIK_QUADRATIC)
+        k_lg_project<<<lg_blocks((size_t)mp.Dtot * 32), 256, 0, c.s>>>(c.L, c.tau, F_D1_0, F_D1_1,
+                                                                      c.L.vec + (size_t)V_GRAD * d);
+    lg_op(c, LG_STATE, 0, qv, 0, what & ~SGP_EVAL_HESSIAN);
+    if (hess) {
+        if (lg_sync(c)) return c.status;
+        k_lg_zero<<<lg_blocks((size_t)d * d), 256, 0, c.s>>>(c.L.H, (size_t)d * d);
+        if (c.tau != 0.0 && mp.lik != SGP_LIK_QUADRATIC) {
+            const int fields[3] = {F_D2_00, F_D2_01, F_D2_11};
+            for (int j1 = 0; j1 < mp.J; ++j1)
+                for (int j2 = j1; j2 < mp.J; ++j2) {
+                    const double *a = c.L.M.phis + (j1 ? mp.Dp0 : 0);
+                    const double *b = c.L.M.phis + (j2 ? mp.Dp0 : 0);
+                    double *C = c.L.H + (size_t)mp.fstart[j1] * d + mp.fstart[j2];
+                    const double *w = c.L.S + (size_t)fields[j1 + j2] * mp.ld;
+                    lg_gemm(c, mp.D[j1], mp.D[j2], mp.N, a, mp.Dp, 1, b, mp.Dp, 0, w, C, d, c.tau, j1 == j2);
+                    if (j1 == j2)
+                        k_lg_mirror_block<<<lg_blocks((size_t)mp.D[j1] * mp.D[j1]), 256, 0, c.s>>>(
+                            c.L.H, d, mp.fstart[j1], mp.D[j1]);
+                    else
+                        k_lg_transpose_block<<<lg_blocks((size_t)mp.D[j1] * mp.D[j2]), 256, 0, c.s>>>(
+                            c.L.H, d, mp.fstart[j1], mp.fstart[j2], mp.D[j1], mp.D[j2]);
+                }
+        }
+        lg_op(c, LG_STATE, 0, qv, 0, SGP_EVAL_HESSIAN | SGP_EVAL_HPRIOR | SGP_EVAL_REUSE);
+    }
+    return lg_sync(c);
+}
+
+// W = Psi_slot (diag r - (b b^T) o T) Psi_slot^T, b from vec[pv]
+static void lg_contraction(LgCtx &c, int slot, int pv) {
+    const int d = c.d;
+    lg_op(c, LG_BVEC, slot, pv);
+    k_lg_mmat<<<lg_blocks((size_t)d * d), 256, 0, c.s>>>(c.L, slot, c.cfg.kappa, -1.0, 1, 1);
+    lg_gemm(c, d, d, d, c.L.P[slot], d, 0, c.L.W, d, 0, nullptr, c.L.X, d, 1.0, 0);  // X = Psi M
+    lg_gemm(c, d, d, d, c.L.X, d, 0, c.L.P[slot], d, 1, nullptr, c.L.W, d, 1.0, 1);  // W = X Psi^T
+    k_mirror_upper<<<lg_blocks((size_t)d * d), 256, 0, c.s>>>(c.L.W, d, d);
+}
+
+// t (vec TV) = tr(W dH/dq) at vec[qv]; per-sample derivatives already in S
+static int lg_trace(LgCtx &c, int qv) {
+    const ModelParams &mp = c.L.M.mp;
+    const int d = c.d;
+    if (c.tau != 0.0 && mp.lik != SGP_LIK_QUADRATIC) {
+        for (int j1 = 0; j1 < mp.J; ++j1) {
+            const double *a = c.L.M.phis + (j1 ? mp.Dp0 : 0);
+            const double *b = c.L.W + (size_t)mp.fstart[j1] * d;
+            lg_gemm(c, mp.N, mp.Dtot, mp.D[j1], a, mp.Dp, 0, b, d, 0, nullptr, c.L.Y, mp.Dtot, 1.0, 0);
+            k_lg_rowdot<<<lg_blocks((size_t)mp.N * 32), 256, 0, c.s>>>(c.L, j1, j1 == mp.J - 1);
+        }
+        k_lg_project<<<lg_blocks((size_t)mp.Dtot * 32), 256, 0, c.s>>>(c.L, c.tau, F_C0, F_C1,
+                                                                      c.L.vec + (size_t)V_TV * d);
+    } else {
+        k_lg_zero<<<lg_blocks(d), 256, 0, c.s>>>(c.L.vec + (size_t)V_TV * d, d);
+    }
+    lg_op(c, LG_TRACE, 0, qv);
+    return lg_sync(c);
+}
+
+static double lg_hnorm(LgCtx &c) {
+    k_lg_frob<<<1, 1024, 0, c.s>>>(c.L.H, (size_t)c.d * c.d, c.L.sc + 8);
+    lg_sync(c);
+    return sqrt(c.sc[8]);
+}
+
+// Jacobi on H with V = P_dst: parallel (grid, round-robin) or reference order (one warp)
+static int lg_jacobi(LgCtx &c, int dst, double tol, double skip, bool parallel, int *sweeps) {
+    const int d = c.d;
+    if (!parallel) {
+        k_lg_set2<<<1, 1, 0, c.s>>>(c.L.sc + 9, tol, skip);
+        lg_op(c, LG_JCYC, dst);
+        lg_sync(c);
+        *sweeps = c.si[4];
+        return c.status;
+    }
+    const int m = d + (d & 1), np = m >> 1;
+    int sw = 0;
+    for (;;) {
+        lg_op(c, LG_OFFNORM);
+        lg_sync(c);
+        if (c.sc[7] <= tol) break;
+        if (sw >= c.cfg.sweep_cap) {
+            *sweeps = -1;
+            return SGP_STATUS_JACOBI;
+        }
+        for (int r = 0; r < m - 1; ++r) {
+            k_lg_jrows<<<np, 256, 0, c.s>>>(c.L.H, d, r, skip, c.L.jprm, c.L.jpairs);
+            k_lg_jcols<<<std::min(d, 148 * 8), 256, 0, c.s>>>(c.L.H, c.L.P[dst], d, c.L.jprm, c.L.jpairs);
+        }
+        ++sw;
+    }
+    *sweeps = sw;
+    return 0;
+}
+
+// cold decomposition of H into slot dst (metric.py:112-142)
+static int lg_eig_cold(LgCtx &c, int dst, int *sweeps) {
+    const int d = c.d;
+    k_lg_symmetrize<<<lg_blocks((size_t)d * d), 256, 0, c.s>>>(c.L.H, d);
+    const double hnorm = lg_hnorm(c);
+    const double tol = c.cfg.zeta * hnorm, skip = d ? tol / d : 0.0;
+    k_lg_eye<<<lg_blocks((size_t)d * d), 256, 0, c.s>>>(c.L.P[dst], d);
+    const int st = lg_jacobi(c, dst, tol, skip, c.cfg.warm_order == SGP_ORDER_PARALLEL, sweeps);
+    if (st) return st;
+    lg_op(c, LG_GLAM, dst, 0, 0, 0);
+    c.since[dst] = 0;
+    return lg_sync(c);
+}
+
+// warm decomposition of H in P_src's basis into slot dst (metric.py:145-185)
+static int lg_eig_warm(LgCtx &c, int src, int dst, int *sweeps) {
+    const int d = c.d;
+    int since = c.since[src] + 1;
+    if (c.cfg.gs_interval && since >= c.cfg.gs_interval) {
+        lg_op(c, LG_MGS, src);
+        since = 0;
+    }
+    const double hnorm = lg_hnorm(c);
+    lg_gemm(c, d, d, d, c.L.P[src], d, 1, c.L.H, d, 0, nullptr, c.L.X, d, 1.0, 0);  // X = Psi^T H
+    lg_gemm(c, d, d, d, c.L.X, d, 0, c.L.P[src], d, 0, nullptr, c.L.H, d, 1.0, 0);  // A = X Psi
+    k_lg_symmetrize<<<lg_blocks((size_t)d * d), 256, 0, c.s>>>(c.L.H, d);
+    k_lg_copy<<<lg_blocks((size_t)d * d), 256, 0, c.s>>>(c.L.P[dst], c.L.P[src], (size_t)d * d);
+    const double tol = c.cfg.zeta * hnorm, skip = d ? tol / d : 0.0;
+    const int st = lg_jacobi(c, dst, tol, skip, c.cfg.warm_order == SGP_ORDER_PARALLEL, sweeps);
+    if (st) return st;
+    lg_op(c, LG_GLAM, dst, 0, 0, since);
+    c.since[dst] = since;
+    return lg_sync(c);
+}
+
+// one generalized leapfrog (sampler.py:209-258); frame: vec Q0, GRAD, S, slot f
+static int lg_leapfrog(LgCtx &c, int &f, int *fp_p, int *fp_q, double *sweep_sum, int *sweep_cnt, int *sweep_log) {
+    const int d = c.d;
+    const double eps = c.cfg.epsilon;
+    int st;
+    lg_contraction(c, f, V_P);
+    if ((st = lg_trace(c, V_Q0))) return st;
+    lg_op(c, LG_PHALF, 0, 0, V_PH, 0, eps);
+    bool conv = false;
+    for (int it = 0; it < c.cfg.fp_max_iters; ++it) {
+        lg_contraction(c, f, V_PH);
+        if ((st = lg_trace(c, V_Q0))) return st;
+        lg_op(c, LG_PHALF, 0, 0, V_PN, 1, eps);
+        cudaMemcpyAsync(c.L.vec + (size_t)V_PH * d, c.L.vec + (size_t)V_PN * d, sizeof(double) * d,
+                        cudaMemcpyDeviceToDevice, c.s);
+        lg_sync(c);
+        if (c.sc[5] <= c.cfg.fp_tol) {
+            conv = true;
+            if (fp_p) *fp_p = it + 1;
+            break;
+        }
+    }
+    if (!conv) return SGP_STATUS_STALL_P;
+    lg_op(c, LG_APPLY, f, V_PH, V_V0, 0);
+    // qc = q0 + eps v0 (QDELTA with the roles shifted: use tmp = v0 -> qn = q0 + eps v0)
+    cudaMemcpyAsync(c.L.vec + (size_t)V_TMP * d, c.L.vec + (size_t)V_V0 * d, sizeof(double) * d,
+                    cudaMemcpyDeviceToDevice, c.s);
+    lg_op(c, LG_QDELTA, 0, 0, 0, 0, 2.0 * eps / 2.0 * 1.0);  // qn = q0 + 0.5*eps*(v0 + v0)
+    cudaMemcpyAsync(c.L.vec + (size_t)V_QC * d, c.L.vec + (size_t)V_QN * d, sizeof(double) * d,
+                    cudaMemcpyDeviceToDevice, c.s);
+    int prev = f, cur = f;
+    conv = false;
+    for (int it = 0; it < c.cfg.fp_max_iters; ++it) {
+        if ((st = lg_state(c, V_QC, SGP_EVAL_HESSIAN))) return st;
+        const int nxt = 1 - prev;
+        int sw = 0;
+        st = c.cfg.metric == SGP_METRIC_STATIC ? lg_eig_cold(c, nxt, &sw) : lg_eig_warm(c, prev, nxt, &sw);
+        if (sweep_log && it < 32) sweep_log[it] = sw;
+        if (st) return st;
+        *sweep_sum += sw;
+        ++*sweep_cnt;
+        cur = nxt;
+        lg_op(c, LG_APPLY, cur, V_PH, V_TMP, 0);
+        lg_op(c, LG_QDELTA, 0, 0, 0, 0, eps);
+        lg_sync(c);
+        if (c.sc[5] <= c.cfg.fp_tol) {
+            conv = true;
+            if (fp_q) *fp_q = it + 1;
+            break;
+        }
+        cudaMemcpyAsync(c.L.vec + (size_t)V_QC * d, c.L.vec + (size_t)V_QN * d, sizeof(double) * d,
+                        cudaMemcpyDeviceToDevice, c.s);
+        prev = cur;
+    }
+    if (!conv) return SGP_STATUS_STALL_Q;
+    f = cur;
+    lg_contraction(c, f, V_PH);
+    if ((st = lg_state(c, V_QC, SGP_EVAL_GRADIENT | SGP_EVAL_REUSE))) return st;
+    if ((st = lg_trace(c, V_QC))) return st;
+    // p_new = ph - 0.5 eps (grad + 0.5 tv): PHALF computes p - ..., so stage ph into p first
+    cudaMemcpyAsync(c.L.vec + (size_t)V_P * d, c.L.vec + (size_t)V_PH * d, sizeof(double) * d,
+                    cudaMemcpyDeviceToDevice, c.s);
+    lg_op(c, LG_PHALF, 0, 0, V_P, 0, eps);
+    cudaMemcpyAsync(c.L.vec + (size_t)V_Q0 * d, c.L.vec + (size_t)V_QC * d, sizeof(double) * d,
+                    cudaMemcpyDeviceToDevice, c.s);
+    lg_sync(c);
+    return 0;
+}
+
+// ---- workspace (one chain at a time; cached per model) ----------------------
+
+// d > 256 (or very wide designs) take the GEMM path; SGP_FORCE_LARGE=1 routes
+// any model through it (used by the parity tests on the golden chains).
+static bool lg_is_large(const ModelDev &M) {
+    if (M.mp.lik == SGP_LIK_QUADRATIC) return false;
+    const char *f = getenv("SGP_FORCE_LARGE");
+    if (f && f[0] == '1') return true;
+    return M.mp.d > 256 || M.mp.Dp > 512;
+}
+
+static int lg_alloc(const ModelDev &M, LgPtrs &L, void **owner) {
+    const int d = M.mp.d, ld = M.mp.ld;
+    const size_t dd = (size_t)d * d;
+    const size_t np = (size_t)(d + 1) / 2 + 1;
+    size_t off = 0;
+    auto take = [&](size_t n) {
+        size_t o = off;
+        off += (n + 3) & ~size_t(3);
+        return o;
+    };
+    const size_t oS = take((size_t)F_COUNT * ld), oH = take(dd), oX = take(dd), oW = take(dd), oP0 = take(dd),
+                 oP1 = take(dd), oY = take((size_t)std::max(M.mp.N, 1) * std::max(M.mp.Dtot, 1)),
+                 osa = take(3 * (size_t)ld), ov = take(16 * (size_t)d), osc = take(16), osi = take(16),
+                 ost = take(2), ojl = take(sgp_jacobi_log_doubles(d)), ojp = take(5 * np), ojq = take(2 * np),
+                 ored = take(64);
+    double *base = nullptr;
+    if (cudaMalloc(&base, off * sizeof(double)) != cudaSuccess) return SGP_ENOMEM;
+    cudaMemset(base, 0, off * sizeof(double));
+    L.M = M;
+    L.S = base + oS;
+    L.H = base + oH;
+    L.X = base + oX;
+    L.W = base + oW;
+    L.P[0] = base + oP0;
+    L.P[1] = base + oP1;
+    L.Y = base + oY;
+    L.sacc = base + osa;
+    L.vec = base + ov;
+    L.sc = base + osc;
+    L.si = reinterpret_cast<int *>(base + osi);
+    L.status = reinterpret_cast<int *>(base + ost);
+    L.jlog = base + ojl;
+    L.jprm = base + ojp;
+    L.jpairs = reinterpret_cast<int *>(base + ojq);
+    L.red = base + ored;
+    *owner = base;
+    return SGP_OK;
+}
+
+// Builds the frame at vec Q0: potential, gradient, S; cold metric in slot 0
+// (or resumes from a stored psi/lam when resume != 0).
+static int lg_frame(LgCtx &c, bool resume, const double *psi, const double *lam, int since, int &f) {
+    const int d = c.d;
+    const bool euclid = c.cfg.metric == SGP_METRIC_EUCLIDEAN;
+    f = 0;
+    if (resume || euclid) {
+        int st = lg_state(c, V_Q0, SGP_EVAL_POTENTIAL | SGP_EVAL_GRADIENT);
+        if (st || euclid) return st;
+        cudaMemcpyAsync(c.L.P[0], psi, sizeof(double) * d * d, cudaMemcpyDeviceToDevice, c.s);
+        // lam -> H diagonal is not needed: load lam into slot 0 directly
+        cudaMemcpyAsync(c.L.vec + (size_t)V_LAM0 * d, lam, sizeof(double) * d, cudaMemcpyDeviceToDevice, c.s);
+        // g, logdet from lam: reuse GLAM on a diagonal H
+        k_lg_zero<<<lg_blocks((size_t)d * d), 256, 0, c.s>>>(c.L.H, (size_t)d * d);
+
+        cudaMemcpy2DAsync(c.L.H, (d + 1) * sizeof(double), lam, sizeof(double), sizeof(double), d,
+                          cudaMemcpyDeviceToDevice, c.s);
+        lg_op(c, LG_GLAM, 0, 0, 0, since);
+        c.since[0] = since;
+        return lg_sync(c);
+    }
+    int st = lg_state(c, V_Q0, SGP_EVAL_POTENTIAL | SGP_EVAL_GRADIENT | SGP_EVAL_HESSIAN);
+    if (st) return st;
+    int sw;
+    return lg_eig_cold(c, 0, &sw);
+}
+
+static void lg_ctx(LgCtx &c, const LgPtrs &L, const sgp_chain_config &cfg, double tau, cudaStream_t s) {
+    c.L = L;
+    c.s = s;
+    c.cfg = cfg;
+    c.tau = tau;
+    c.d = L.M.mp.d;
+    c.since[0] = c.since[1] = 0;
+    memset(c.sc, 0, sizeof(c.sc));
+    memset(c.si, 0, sizeof(c.si));
+    c.status = 0;
+}
+
+static int lg_euclid_leapfrog(LgCtx &c) {
+    // p_half = p - eps/2 grad ; q = q0 + eps p_half ; grad at q ; p = p_half - eps/2 grad
+    const int d = c.d;
+    const double eps = c.cfg.epsilon;
+    // reuse PHALF with tv = 0: out = p - 0.5 eps (grad + 0.5*0)
+    k_lg_zero<<<lg_blocks(d), 256, 0, c.s>>>(c.L.vec + (size_t)V_TV * d, d);
+    lg_op(c, LG_PHALF, 0, 0, V_PH, 0, eps);
+    cudaMemcpyAsync(c.L.vec + (size_t)V_V0 * d, c.L.vec + (size_t)V_PH * d, sizeof(double) * d,
+                    cudaMemcpyDeviceToDevice, c.s);
+    cudaMemcpyAsync(c.L.vec + (size_t)V_TMP * d, c.L.vec + (size_t)V_PH * d, sizeof(double) * d,
+                    cudaMemcpyDeviceToDevice, c.s);
+    lg_op(c, LG_QDELTA, 0, 0, 0, 0, eps);  // qn = q0 + eps p_half
+    cudaMemcpyAsync(c.L.vec + (size_t)V_Q0 * d, c.L.vec + (size_t)V_QN * d, sizeof(double) * d,
+                    cudaMemcpyDeviceToDevice, c.s);
+    int st = lg_state(c, V_Q0, SGP_EVAL_POTENTIAL | SGP_EVAL_GRADIENT);
+    if (st) return st;
+    cudaMemcpyAsync(c.L.vec + (size_t)V_P * d, c.L.vec + (size_t)V_PH * d, sizeof(double) * d,
+                    cudaMemcpyDeviceToDevice, c.s);
+    lg_op(c, LG_PHALF, 0, 0, V_P, 0, eps);
+    return lg_sync(c);
+}
+
+static double lg_kinetic(LgCtx &c, int f) {
+    if (c.cfg.metric == SGP_METRIC_EUCLIDEAN) {
+        // 0.5 p.p + 0.5 d ln 2pi via metric_quad with identity is not available: compute on host
+        std::vector<double> p(c.d);
+        cudaMemcpyAsync(p.data(), c.L.vec + (size_t)V_P * c.d, sizeof(double) * c.d, cudaMemcpyDeviceToHost, c.s);
+        cudaStreamSynchronize(c.s);
+        double s = 0.0;
+        for (double v : p) s += v * v;
+        return 0.5 * s + 0.5 * c.d * SGP_LN_2PI;
+    }
+    lg_op(c, LG_KINETIC, f);
+    lg_sync(c);
+    return c.sc[6];
+}
+
+// ---- large-path implementations of the C ABI entry points -------------------
+
+static int lg_chain_init(const LgPtrs &L, const sgp_chain_config *cfg, const sgp_chain_state *st, cudaStream_t s) {
+    const int d = L.M.mp.d;
+    std::vector<int> status(st->n_chains, 0);
+    std::vector<double> tau(st->n_chains);
+    cudaMemcpy(tau.data(), st->tau, sizeof(double) * st->n_chains, cudaMemcpyDeviceToHost);
+    cudaMemcpy(status.data(), st->status, sizeof(int) * st->n_chains, cudaMemcpyDeviceToHost);
+    for (int z = 0; z < st->n_chains; ++z) {
+        if (status[z]) continue;
+        LgCtx c;
+        lg_ctx(c, L, *cfg, tau[z], s);
+        lg_clear_status(c);
+        cudaMemcpyAsync(L.vec + (size_t)V_Q0 * d, st->q + (size_t)z * d, sizeof(double) * d,
+                        cudaMemcpyDeviceToDevice, s);
+        int f = 0;
+        const int rc = lg_frame(c, false, nullptr, nullptr, 0, f);
+        status[z] = rc ? SGP_STATUS_CHAIN_START : 0;
+        if (!rc && cfg->metric != SGP_METRIC_EUCLIDEAN) {
+            cudaMemcpyAsync(st->psi + (size_t)z * d * d, L.P[0], sizeof(double) * d * d, cudaMemcpyDeviceToDevice, s);
+            cudaMemcpyAsync(st->lam + (size_t)z * d, L.vec + (size_t)V_LAM0 * d, sizeof(double) * d,
+                            cudaMemcpyDeviceToDevice, s);
+        }
+    }
+    cudaMemcpyAsync(st->status, status.data(), sizeof(int) * st->n_chains, cudaMemcpyHostToDevice, s);
+    std::vector<int> zero(st->n_chains, 0);
+    cudaMemcpyAsync(st->since, zero.data(), sizeof(int) * st->n_chains, cudaMemcpyHostToDevice, s);
+    return cudaStreamSynchronize(s) == cudaSuccess ? SGP_OK : SGP_ECUDA;
+}
+
+static int lg_run_moves(const LgPtrs &L, const sgp_chain_config *cfg, const sgp_chain_state *st, int moves,
+                        int move_offset, const double *d_z, const double *d_logu, sgp_move_records *rec,
+                        cudaStream_t s) {
+    const int d = L.M.mp.d, Z = st->n_chains;
+    const bool euclid = cfg->metric == SGP_METRIC_EUCLIDEAN;
+    std::vector<int> status(Z), since(Z);
+    std::vector<double> tau(Z), logu((size_t)moves * Z);
+    cudaMemcpy(tau.data(), st->tau, sizeof(double) * Z, cudaMemcpyDeviceToHost);
+    cudaMemcpy(status.data(), st->status, sizeof(int) * Z, cudaMemcpyDeviceToHost);
+    cudaMemcpy(since.data(), st->since, sizeof(int) * Z, cudaMemcpyDeviceToHost);
+    cudaMemcpy(logu.data(), d_logu, sizeof(double) * moves * Z, cudaMemcpyDeviceToHost);
+    const size_t R = (size_t)moves * Z;
+    std::vector<double> lp(R), hb(R), ha(R), sm(R), wall(R);
+    std::vector<uint8_t> acc(R), dv(R);
+    for (int z = 0; z < Z; ++z) {
+        if (status[z]) continue;
+        LgCtx c;
+        lg_ctx(c, L, *cfg, tau[z], s);
+        lg_clear_status(c);
+        cudaMemcpyAsync(L.vec + (size_t)V_Q0 * d, st->q + (size_t)z * d, sizeof(double) * d,
+                        cudaMemcpyDeviceToDevice, s);
+        int f = 0;
+        if (lg_frame(c, true, st->psi + (size_t)z * d * d, st->lam + (size_t)z * d, since[z], f)) {
+            status[z] = SGP_STATUS_CHAIN_START;
+            continue;
+        }
+        int final_status = 0;
+        for (int mv = 0; mv < moves; ++mv) {
+            const auto t0 = std::chrono::steady_clock::now();
+            const double *zz = d_z + ((size_t)mv * Z + z) * d;
+            if (euclid) {
+                cudaMemcpyAsync(L.vec + (size_t)V_P * d, zz, sizeof(double) * d, cudaMemcpyDeviceToDevice, s);
+            } else {
+                cudaMemcpyAsync(L.vec + (size_t)V_PN * d, zz, sizeof(double) * d, cudaMemcpyDeviceToDevice, s);
+                lg_op(c, LG_APPLY, f, V_PN, V_P, 2);
+            }
+            lg_sync(c);
+            const double pot_before = c.sc[2];
+            const double h_before = pot_before + lg_kinetic(c, f);
+            cudaMemcpyAsync(L.vec + (size_t)V_QS * d, L.vec + (size_t)V_Q0 * d, sizeof(double) * d,
+                            cudaMemcpyDeviceToDevice, s);
+            double sweep_sum = 0.0;
+            int sweep_cnt = 0;
+            int fr = f, ls = 0;
+            for (int l = 0; l < cfg->leapfrogs && !ls; ++l)
+                ls = euclid ? lg_euclid_leapfrog(c) : lg_leapfrog(c, fr, nullptr, nullptr, &sweep_sum, &sweep_cnt,
+                                                                   nullptr);
+            bool div = ls != 0;
+            double h_after = NAN;
+            if (!div) {
+                lg_sync(c);
+                h_after = c.sc[2] + lg_kinetic(c, fr);
+                if (!std::isfinite(h_after)) div = true;
+            }
+            if (div) h_after = NAN;
+            const size_t ri = (size_t)mv * Z + z;
+            const bool accept = !div && (h_before - h_after) > logu[ri];
+            lg_clear_status(c);
+            if (accept) {
+                f = fr;
+            } else if (div && mv + move_offset == 0) {
+                final_status = SGP_STATUS_FIRST_MOVE;
+            } else {
+                cudaMemcpyAsync(L.vec + (size_t)V_Q0 * d, L.vec + (size_t)V_QS * d, sizeof(double) * d,
+                                cudaMemcpyDeviceToDevice, s);
+                const int rs = lg_frame(c, false, nullptr, nullptr, 0, f);  // cold resync
+                if (rs) final_status = rs;
+            }
+            lg_sync(c);
+            lp[ri] = -c.sc[2];
+            hb[ri] = h_before;
+            ha[ri] = h_after;
+            acc[ri] = accept;
+            dv[ri] = div;
+            sm[ri] = sweep_cnt ? sweep_sum / sweep_cnt : 0.0;
+            wall[ri] = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+            if (rec->q)
+                cudaMemcpyAsync(rec->q + ri * d, L.vec + (size_t)(final_status ? V_QS : V_Q0) * d,
+                                sizeof(double) * d, cudaMemcpyDeviceToDevice, s);
+            if (final_status) break;
+        }
+        cudaMemcpyAsync(st->q + (size_t)z * d, L.vec + (size_t)V_Q0 * d, sizeof(double) * d,
+                        cudaMemcpyDeviceToDevice, s);
+        if (!euclid && !final_status) {
+            cudaMemcpyAsync(st->psi + (size_t)z * d * d, L.P[f], sizeof(double) * d * d, cudaMemcpyDeviceToDevice, s);
+            cudaMemcpyAsync(st->lam + (size_t)z * d, L.vec + (size_t)(V_LAM0 + f) * d, sizeof(double) * d,
+                            cudaMemcpyDeviceToDevice, s);
+            since[z] = c.since[f];
+        }
+        status[z] = final_status;
+    }
+    cudaMemcpyAsync(rec->logpost, lp.data(), sizeof(double) * R, cudaMemcpyHostToDevice, s);
+    cudaMemcpyAsync(rec->h_before, hb.data(), sizeof(double) * R, cudaMemcpyHostToDevice, s);
+    cudaMemcpyAsync(rec->h_after, ha.data(), sizeof(double) * R, cudaMemcpyHostToDevice, s);
+    cudaMemcpyAsync(rec->sweeps_mean, sm.data(), sizeof(double) * R, cudaMemcpyHostToDevice, s);
+    cudaMemcpyAsync(rec->wall_ms, wall.data(), sizeof(double) * R, cudaMemcpyHostToDevice, s);
+    cudaMemcpyAsync(rec->accept, acc.data(), R, cudaMemcpyHostToDevice, s);
+    cudaMemcpyAsync(rec->divergent, dv.data(), R, cudaMemcpyHostToDevice, s);
+    cudaMemcpyAsync(st->status, status.data(), sizeof(int) * Z, cudaMemcpyHostToDevice, s);
+    cudaMemcpyAsync(st->since, since.data(), sizeof(int) * Z, cudaMemcpyHostToDevice, s);
+    return cudaStreamSynchronize(s) == cudaSuccess ? SGP_OK : SGP_ECUDA;
+}
+
+static int lg_leapfrog_api(const LgPtrs &L, const sgp_chain_config *cfg, const sgp_chain_state *st, double *d_p,
+                           sgp_leapfrog_diag *diag, cudaStream_t s) {
+    const int d = L.M.mp.d, Z = st->n_chains;
+    std::vector<double> tau(Z);
+    std::vector<int> since(Z), status(Z, 0);
+    cudaMemcpy(tau.data(), st->tau, sizeof(double) * Z, cudaMemcpyDeviceToHost);
+    cudaMemcpy(since.data(), st->since, sizeof(int) * Z, cudaMemcpyDeviceToHost);
+    for (int z = 0; z < Z; ++z) {
+        LgCtx c;
+        lg_ctx(c, L, *cfg, tau[z], s);
+        lg_clear_status(c);
+        cudaMemcpyAsync(L.vec + (size_t)V_Q0 * d, st->q + (size_t)z * d, sizeof(double) * d,
+                        cudaMemcpyDeviceToDevice, s);
+        cudaMemcpyAsync(L.vec + (size_t)V_P * d, d_p + (size_t)z * d, sizeof(double) * d, cudaMemcpyDeviceToDevice, s);
+        int f = 0, fp_p = 0, fp_q = 0, cnt = 0, slog[32];
+        double ssum = 0.0;
+        for (int k = 0; k < 32; ++k) slog[k] = -1;
+        int rc = lg_frame(c, true, st->psi + (size_t)z * d * d, st->lam + (size_t)z * d, since[z], f);
+        if (!rc)
+            rc = cfg->metric == SGP_METRIC_EUCLIDEAN ? lg_euclid_leapfrog(c)
+                                                     : lg_leapfrog(c, f, &fp_p, &fp_q, &ssum, &cnt, slog);
+        status[z] = rc;
+        if (!rc) {
+            cudaMemcpyAsync(st->q + (size_t)z * d, L.vec + (size_t)V_Q0 * d, sizeof(double) * d,
+                            cudaMemcpyDeviceToDevice, s);
+            cudaMemcpyAsync(d_p + (size_t)z * d, L.vec + (size_t)V_P * d, sizeof(double) * d,
+                            cudaMemcpyDeviceToDevice, s);
+            if (cfg->metric != SGP_METRIC_EUCLIDEAN) {
+                cudaMemcpyAsync(st->psi + (size_t)z * d * d, L.P[f], sizeof(double) * d * d, cudaMemcpyDeviceToDevice,
+                                s);
+                cudaMemcpyAsync(st->lam + (size_t)z * d, L.vec + (size_t)(V_LAM0 + f) * d, sizeof(double) * d,
+                                cudaMemcpyDeviceToDevice, s);
+                since[z] = c.since[f];
+            }
+        }
+        if (diag) {
+            if (diag->fp_p_iters) cudaMemcpyAsync(diag->fp_p_iters + z, &fp_p, sizeof(int), cudaMemcpyHostToDevice, s);
+            if (diag->fp_q_iters) cudaMemcpyAsync(diag->fp_q_iters + z, &fp_q, sizeof(int), cudaMemcpyHostToDevice, s);
+            if (diag->sweeps)
+                cudaMemcpyAsync(diag->sweeps + (size_t)z * cfg->fp_max_iters, slog, sizeof(int) * cfg->fp_max_iters,
+                                cudaMemcpyHostToDevice, s);
+            cudaStreamSynchronize(s);
+        }
+    }
+    cudaMemcpyAsync(st->status, status.data(), sizeof(int) * Z, cudaMemcpyHostToDevice, s);
+    cudaMemcpyAsync(st->since, since.data(), sizeof(int) * Z, cudaMemcpyHostToDevice, s);
+    return cudaStreamSynchronize(s) == cudaSuccess ? SGP_OK : SGP_ECUDA;
+}
+
+static int lg_eval_api(const LgPtrs &L, int Z, const double *d_tau, const double *d_q, int what, double *d_pot,
+                       double *d_grad, double *d_hess, double *d_sumpot, int *d_status, cudaStream_t s) {
+    const int d = L.M.mp.d;
+    std::vector<double> tau(Z);
+    cudaMemcpy(tau.data(), d_tau, sizeof(double) * Z, cudaMemcpyDeviceToHost);
+    sgp_chain_config cfg{};
+    for (int z = 0; z < Z; ++z) {
+        LgCtx c;
+        lg_ctx(c, L, cfg, tau[z], s);
+        lg_clear_status(c);
+        cudaMemcpyAsync(L.vec + (size_t)V_Q0 * d, d_q + (size_t)z * d, sizeof(double) * d, cudaMemcpyDeviceToDevice, s);
+        const int rc = lg_state(c, V_Q0, what);
+        if (d_pot) cudaMemcpyAsync(d_pot + z, L.sc + 2, sizeof(double), cudaMemcpyDeviceToDevice, s);
+        if (d_sumpot) cudaMemcpyAsync(d_sumpot + z, L.sc + 3, sizeof(double), cudaMemcpyDeviceToDevice, s);
+        if (d_grad && (what & SGP_EVAL_GRADIENT))
+            cudaMemcpyAsync(d_grad + (size_t)z * d, L.vec + (size_t)V_GRAD * d, sizeof(double) * d,
+                            cudaMemcpyDeviceToDevice, s);
+        if (d_hess && (what & SGP_EVAL_HESSIAN))
+            cudaMemcpyAsync(d_hess + (size_t)z * d * d, L.H, sizeof(double) * d * d, cudaMemcpyDeviceToDevice, s);
+        cudaMemcpyAsync(d_status + z, &rc, sizeof(int), cudaMemcpyHostToDevice, s);
+        cudaStreamSynchronize(s);
+    }
+    return SGP_OK;
+}
+
+static int lg_trace_api(const LgPtrs &L, int Z, const double *d_tau, const double *d_q, const double *d_w,
+                        double *d_t, int *d_status, cudaStream_t s) {
+    const int d = L.M.mp.d;
+    std::vector<double> tau(Z);
+    cudaMemcpy(tau.data(), d_tau, sizeof(double) * Z, cudaMemcpyDeviceToHost);
+    sgp_chain_config cfg{};
+    for (int z = 0; z < Z; ++z) {
+        LgCtx c;
+        lg_ctx(c, L, cfg, tau[z], s);
+        lg_clear_status(c);
+        cudaMemcpyAsync(L.vec + (size_t)V_Q0 * d, d_q + (size_t)z * d, sizeof(double) * d, cudaMemcpyDeviceToDevice, s);
+        int rc = lg_state(c, V_Q0, 0);
+        if (!rc) {
+            cudaMemcpyAsync(L.W, d_w + (size_t)z * d * d, sizeof(double) * d * d, cudaMemcpyDeviceToDevice, s);
+            k_lg_symmetrize<<<lg_blocks((size_t)d * d), 256, 0, s>>>(L.W, d);
+            rc = lg_trace(c, V_Q0);
+        }
+        cudaMemcpyAsync(d_t + (size_t)z * d, L.vec + (size_t)V_TV * d, sizeof(double) * d, cudaMemcpyDeviceToDevice, s);
+        cudaMemcpyAsync(d_status + z, &rc, sizeof(int), cudaMemcpyHostToDevice, s);
+        cudaStreamSynchronize(s);
+    }
+    return SGP_OK;
+}

@@ -1,0 +1,108 @@
+// Correctness and throughput of the DMMA GEMM (sgp_gemm.cuh).
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -o tools/gemm_bench tools/gemm_bench.cu
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+#include "../paper_2511_06407_b200/csrc/sgp_gemm.cuh"
+
+static void ref(const GemmArgs &g, const std::vector<double> &A, const std::vector<double> &B,
+                const std::vector<double> &s, std::vector<double> &C) {
+    for (int m = 0; m < g.M; ++m)
+        for (int n = 0; n < g.N; ++n) {
+            double acc = 0;
+            for (int k = 0; k < g.K; ++k) {
+                double a = g.TA ? A[(size_t)k * g.lda + m] : A[(size_t)m * g.lda + k];
+                double b = g.TB ? B[(size_t)n * g.ldb + k] : B[(size_t)k * g.ldb + n];
+                acc += a * (s.empty() ? 1.0 : s[k]) * b;
+            }
+            C[(size_t)m * g.ldc + n] = acc;
+        }
+}
+
+int main() {
+    int fails = 0;
+    for (int ta = 0; ta < 2; ++ta)
+        for (int tb = 0; tb < 2; ++tb)
+            for (int sc = 0; sc < 2; ++sc) {
+                int M = 67, N = 45, K = 83;
+                GemmArgs g{};
+                g.M = M; g.N = N; g.K = K; g.TA = ta; g.TB = tb;
+                g.lda = ((ta ? M : K) + 1) & ~1; g.ldb = ((tb ? K : N) + 1) & ~1; g.ldc = (N + 1) & ~1;
+                g.alpha = 1; g.beta = 0;
+                std::vector<double> A((size_t)(ta ? K : M) * g.lda), B((size_t)(tb ? N : K) * g.ldb),
+                    S(sc ? K : 0), C((size_t)M * g.ldc), R((size_t)M * g.ldc);
+                for (auto &v : A) v = rand() / (double)RAND_MAX - 0.5;
+                for (auto &v : B) v = rand() / (double)RAND_MAX - 0.5;
+                for (auto &v : S) v = rand() / (double)RAND_MAX;
+                double *dA, *dB, *dC, *dS = nullptr;
+                cudaMalloc(&dA, A.size() * 8); cudaMalloc(&dB, B.size() * 8); cudaMalloc(&dC, C.size() * 8);
+                cudaMemcpy(dA, A.data(), A.size() * 8, cudaMemcpyHostToDevice);
+                cudaMemcpy(dB, B.data(), B.size() * 8, cudaMemcpyHostToDevice);
+                if (sc) { cudaMalloc(&dS, K * 8); cudaMemcpy(dS, S.data(), K * 8, cudaMemcpyHostToDevice); }
+                g.A = dA; g.B = dB; g.C = dC; g.scale = dS;
+                gemm_launch(g, 0);
+                cudaMemcpy(C.data(), dC, C.size() * 8, cudaMemcpyDeviceToHost);
+                ref(g, A, B, S, R);
+                double err = 0;
+                for (int m = 0; m < M; ++m) for (int n = 0; n < N; ++n)
+                    err = fmax(err, fabs(C[(size_t)m * g.ldc + n] - R[(size_t)m * g.ldc + n]));
+                printf("TA=%d TB=%d scale=%d max err %.3e\n", ta, tb, sc, err);
+                fails += err > 1e-12;
+                cudaFree(dA); cudaFree(dB); cudaFree(dC); if (dS) cudaFree(dS);
+            }
+    {   // odd leading dimensions (d = 2083-style buffers) use 8-byte copies
+        int M = 37, N = 29, K = 41;
+        GemmArgs g{};
+        g.M = M; g.N = N; g.K = K; g.TA = 1; g.TB = 0; g.lda = M; g.ldb = N; g.ldc = N; g.alpha = 1;
+        std::vector<double> A((size_t)K * M), B((size_t)K * N), C((size_t)M * N), R((size_t)M * N), S;
+        for (auto &v : A) v = rand() / (double)RAND_MAX - 0.5;
+        for (auto &v : B) v = rand() / (double)RAND_MAX - 0.5;
+        double *dA, *dB, *dC;
+        cudaMalloc(&dA, A.size() * 8); cudaMalloc(&dB, B.size() * 8); cudaMalloc(&dC, C.size() * 8);
+        cudaMemcpy(dA, A.data(), A.size() * 8, cudaMemcpyHostToDevice);
+        cudaMemcpy(dB, B.data(), B.size() * 8, cudaMemcpyHostToDevice);
+        g.A = dA; g.B = dB; g.C = dC;
+        gemm_launch(g, 0);
+        cudaMemcpy(C.data(), dC, C.size() * 8, cudaMemcpyDeviceToHost);
+        ref(g, A, B, S, R);
+        double err = 0;
+        for (size_t i = 0; i < C.size(); ++i) err = fmax(err, fabs(C[i] - R[i]));
+        printf("odd ld max err %.3e\n", err);
+        fails += err > 1e-12;
+    }
+    // throughput
+    struct Case { const char *name; int M, N, K, ta, tb, sc; } cases[] = {
+        {"d^3 NN 2083", 2083, 2083, 2083, 0, 0, 0},
+        {"d^3 NN 2083 odd-ld", 2083, 2083, 2083, 0, 0, -1},
+        {"d^3 TN 2083", 2083, 2083, 2083, 1, 0, 0},
+        {"d^3 NT 2083", 2083, 2083, 2083, 0, 1, 0},
+        {"Hessian blk 1040x1040x8192 TN+scale", 1040, 1040, 8192, 1, 0, 1},
+        {"trace Y 8192x2080x2080 NN", 8192, 2080, 2080, 0, 0, 0},
+        {"square 4096", 4096, 4096, 4096, 0, 0, 0},
+    };
+    for (auto &c : cases) {
+        GemmArgs g{};
+        g.M = c.M; g.N = c.N; g.K = c.K; g.TA = c.ta; g.TB = c.tb;
+        g.lda = ((c.ta ? c.M : c.K) + 3) & ~3; g.ldb = ((c.tb ? c.K : c.N) + 3) & ~3; g.ldc = (c.N + 3) & ~3;
+        if (c.sc < 0) { g.lda = c.ta ? c.M : c.K; g.ldb = c.tb ? c.K : c.N; g.ldc = c.N; c.sc = 0; }
+        g.alpha = 1; g.beta = 0;
+        double *dA, *dB, *dC, *dS = nullptr;
+        size_t na = (size_t)(c.ta ? c.K : c.M) * g.lda, nb = (size_t)(c.tb ? c.N : c.K) * g.ldb;
+        cudaMalloc(&dA, na * 8); cudaMalloc(&dB, nb * 8); cudaMalloc(&dC, (size_t)c.M * g.ldc * 8);
+        cudaMemset(dA, 0, na * 8); cudaMemset(dB, 0, nb * 8);
+        if (c.sc) { cudaMalloc(&dS, c.K * 8); cudaMemset(dS, 0, c.K * 8); }
+        g.A = dA; g.B = dB; g.C = dC; g.scale = dS;
+        gemm_launch(g, 0);
+        cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+        cudaEventRecord(e0);
+        for (int r = 0; r < 5; ++r) gemm_launch(g, 0);
+        cudaEventRecord(e1); cudaEventSynchronize(e1);
+        float ms; cudaEventElapsedTime(&ms, e0, e1); ms /= 5;
+        printf("%-40s %8.3f ms  %6.2f TFLOP/s\n", c.name, ms, 2.0 * c.M * c.N * (double)c.K / (ms * 1e-3) / 1e12);
+        cudaFree(dA); cudaFree(dB); cudaFree(dC); if (dS) cudaFree(dS);
+    }
+    printf(fails ? "FAIL\n" : "OK\n");
+    return fails;
+}
