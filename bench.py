@@ -209,6 +209,37 @@ def measure_dgemm_tflops(torch):
     return 2.0 * n ** 3 / best / 1e12
 
 
+def measure_ess(target, sm_count, args, torch):
+    """min-ESS per chain-move of the C2 sampler: one wave of
+    chains from q = 0, burn-in moves, then recorded moves in one launch; Geyer
+    ESS per coordinate of q, min over coordinates, mean over chains."""
+    from paper_2511_06407_b200.diagnostics import min_ess
+    from paper_2511_06407_b200.sampler import ChainConfig, DeviceChains
+
+    d = target.dim
+    Z = sm_count * args.ess_chains_per_sm
+    cfg = ChainConfig(epsilon=EPS, leapfrogs=LEAPFROGS, moves=1, burnin=0, warm_order=args.warm_order)
+    ch = DeviceChains(target.device, np.ones(Z), cfg)
+    ch.set_q(np.zeros((Z, d)))
+    ch.init()
+    rng = np.random.default_rng(12345)
+    B, M = args.ess_burnin, args.ess_moves
+    t0 = time.perf_counter()
+    with np.errstate(divide="ignore"):
+        if B > 0:
+            ch.run(B, rng.standard_normal((B, Z, d)), np.log(rng.uniform(size=(B, Z))))
+        bufs = ch.run(M, rng.standard_normal((M, Z, d)), np.log(rng.uniform(size=(M, Z))), record_q=True)
+    q = bufs["q"].cpu().numpy()  # (M, Z, d)
+    wall = time.perf_counter() - t0
+    per_chain = np.array([min_ess(q[:, z, :]) for z in range(Z)])
+    return {"chains": Z, "burnin_moves": B, "recorded_moves": M,
+            "min_ess_per_chain_move": float(per_chain.mean() / M),
+            "min_ess_chain_median": float(np.median(per_chain)),
+            "acceptance": float(bufs["accept"].float().mean().item()),
+            "estimator": "Geyer initial-monotone per coordinate of q, min over coordinates, mean over chains",
+            "pilot_wall_s": wall}
+
+
 def run_gpu(args):
     import torch
     import torch.distributed as dist
@@ -322,6 +353,10 @@ def run_gpu(args):
     h2d = Z * d * 8 + Z * 8
     d2h = 3 * Z * 8 + Z + Z * d * 8
 
+    ess = None
+    if rank == 0 and args.ess_moves > 0:
+        ess = measure_ess(target, sm_count, args, torch)
+
     if rank == 0:
         N, D = N_ROWS, d - 3
         F = canonical_flops_per_leapfrog(N, D, d, s=max(1.0, sweeps))
@@ -350,6 +385,10 @@ def run_gpu(args):
             "clocks": clocks.summary(),
             "wall_s_timed": t_wall,
         }
+        if ess is not None:
+            # chain-moves/s of the timed region x ESS per chain-move of the pilot
+            ess["min_ess_per_s"] = ess["min_ess_per_chain_move"] * value / LEAPFROGS
+            line["min_ess"] = ess
         if os.path.exists(peaks_path):
             line["roofline"]["peaks_file"] = "MEASURED_PEAKS.json present (bf16/HBM only)"
         if world == 1 and not args.no_cpu_baseline:
@@ -360,6 +399,8 @@ def run_gpu(args):
             line["cpu_baseline"] = {"value": n / wall, "unit": UNIT, "cores": cores, "kind": "port",
                                     "sample": f"{cores} processes x {args.ref_leapfrogs} generalized "
                                               f"leapfrogs (oracle port, OPENBLAS_NUM_THREADS=1)"}
+            if ess is not None:
+                ess["cpu_min_ess_per_s"] = ess["min_ess_per_chain_move"] * (n / wall) / LEAPFROGS
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
@@ -376,6 +417,9 @@ def main():
     ap.add_argument("--warm-order", default="cyclic", choices=["cyclic", "parallel"])
     ap.add_argument("--ref-leapfrogs", type=int, default=20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ess-moves", type=int, default=120, help="recorded moves of the min-ESS pilot (0: skip)")
+    ap.add_argument("--ess-burnin", type=int, default=30)
+    ap.add_argument("--ess-chains-per-sm", type=int, default=2)
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

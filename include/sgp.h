@@ -232,6 +232,13 @@ int sgp_run_moves(const sgp_model *model, const sgp_chain_config *cfg,
  * 4 Psi^T H Psi, 5 warm Jacobi, 8 cold Jacobi, 9 whole leapfrog. */
 int sgp_debug_phase_cycles(unsigned long long *h_out16, int reset);
 
+/* Self-check of the branch-free fp64 div/sqrt/rcp fast paths the cyclic
+ * Jacobi uses (sgp_core.cuh) against the CUDA library calls on n random
+ * samples: h_counts4 = {rotation (c,s,t) bitwise mismatches on the fast path,
+ * rotations sent to the library path, primitive mismatches on random bit
+ * patterns, n}.  Both mismatch counts must be 0. */
+int sgp_debug_rotation_check(long long n, unsigned long long seed, long long *h_counts4);
+
 /* Device properties the host reports (SM count, name) and library version. */
 int sgp_device_info(int *sm_count, int *cc_major, int *cc_minor);
 const char *sgp_version(void);

@@ -145,6 +145,8 @@ def lib():
                               vp, ctypes.POINTER(MoveRecords), vp]),
         "sgp_device_info": (i, [c_ip, c_ip, c_ip]),
         "sgp_version": (ctypes.c_char_p, []),
+        "sgp_debug_phase_cycles": (i, [vp, i]),
+        "sgp_debug_rotation_check": (i, [ctypes.c_longlong, ctypes.c_ulonglong, vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

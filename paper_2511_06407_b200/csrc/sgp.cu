@@ -872,3 +872,71 @@ extern "C" int sgp_debug_phase_cycles(unsigned long long *h_out16, int reset) {
     }
     return SGP_OK;
 }
+
+// ---------------------------------------------------------------------------
+// Self-check of the branch-free fast paths (sgp_core.cuh) against the library
+// calls: counts[0] rotations whose (c, s, t) differ bitwise although the fast
+// path reported success, counts[1] rotations routed to the library path,
+// counts[2] div/sqrt/rcp results that differ on random bit patterns although
+// the fast path reported success, counts[3] total samples.
+__device__ __forceinline__ unsigned long long sgp_mix64(unsigned long long x) {
+    x += 0x9e3779b97f4a7c15ull;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+    return x ^ (x >> 31);
+}
+__device__ __forceinline__ double sgp_u01(unsigned long long x) { return (double)(x >> 11) * 0x1.0p-53; }
+
+__global__ void k_rotation_check(long long n, unsigned long long seed, unsigned long long *cnt) {
+    unsigned long long bad = 0, slow = 0, badop = 0;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const unsigned long long h0 = sgp_mix64(seed ^ (unsigned long long)i), h1 = sgp_mix64(h0), h2 = sgp_mix64(h1),
+                                 h3 = sgp_mix64(h2), h4 = sgp_mix64(h3);
+        // Jacobi-like operands: diagonal entries over 8 decades, pivots over 20
+        double app = (sgp_u01(h0) < 0.5 ? -1.0 : 1.0) * exp10(8.0 * sgp_u01(h1) - 3.0);
+        double aqq = (h2 & 1) ? app * (1.0 + 1e-9 * (sgp_u01(h2) - 0.5)) : (sgp_u01(h2) - 0.5) * exp10(8.0 * sgp_u01(h3) - 3.0);
+        const double apq = ((h4 & 2) ? -1.0 : 1.0) * exp10(20.0 * sgp_u01(h4) - 16.0);
+        if ((h0 & 0xff) == 7) aqq = app;  // theta = 0
+        double c0, s0, t0, c1, s1, t1;
+        jacobi_rot(app, aqq, apq, c0, s0, t0);
+        if (jacobi_rot_fast(app, aqq, apq, c1, s1, t1)) {
+            if (__double_as_longlong(c0) != __double_as_longlong(c1) || __double_as_longlong(s0) != __double_as_longlong(s1) ||
+                __double_as_longlong(t0) != __double_as_longlong(t1))
+                ++bad;
+        } else {
+            ++slow;
+        }
+        // raw bit patterns (any sign / exponent) for the three primitives
+        const double a = __longlong_as_double((long long)h1), b = __longlong_as_double((long long)h3);
+        bool ok = true;
+        double v = ddiv_fast(a, b, ok);
+        if (ok && __double_as_longlong(v) != __double_as_longlong(__ddiv_rn(a, b))) ++badop;
+        const double x = fabs(a);
+        ok = true;
+        v = dsqrt_fast(x, ok);
+        if (ok && __double_as_longlong(v) != __double_as_longlong(__dsqrt_rn(x))) ++badop;
+        ok = true;
+        v = drcp_fast(b, ok);
+        if (ok && __double_as_longlong(v) != __double_as_longlong(__drcp_rn(b))) ++badop;
+    }
+    atomicAdd(&cnt[0], bad);
+    atomicAdd(&cnt[1], slow);
+    atomicAdd(&cnt[2], badop);
+}
+
+extern "C" int sgp_debug_rotation_check(long long n, unsigned long long seed, long long *h_counts4) {
+    if (!h_counts4 || n < 0) return SGP_EINVAL;
+    unsigned long long *d = nullptr;
+    CUDA_TRY(cudaMalloc(&d, 3 * sizeof(unsigned long long)));
+    CUDA_TRY(cudaMemset(d, 0, 3 * sizeof(unsigned long long)));
+    k_rotation_check<<<148 * 8, 256>>>(n, seed, d);
+    unsigned long long h[3];
+    cudaError_t e = cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    if (e != cudaSuccess) return SGP_ECUDA;
+    h_counts4[0] = (long long)h[0];
+    h_counts4[1] = (long long)h[1];
+    h_counts4[2] = (long long)h[2];
+    h_counts4[3] = n;
+    return SGP_OK;
+}

@@ -318,6 +318,7 @@ __device__ __noinline__ void trace_lik_tiled(EvalCtx &E, const double *Wp) {
     __syncthreads();
 }
 
+
 // ---------------------------------------------------------------------------
 // Full evaluation at q.  what: SGP_EVAL_* bits.  Writes *pot (potential),
 // *sumpot (sum_i U_i), grad[d], H[d*d] as requested.  Status via E.status.
@@ -375,6 +376,7 @@ __device__ __noinline__ void eval_state(EvalCtx &E, const double *q, double tau,
         su = E.su_ext;
         o.sumpot = su;
     } else if (need_lik && !reuse) {
+        SGP_PROF(14);
         su = eval_lik(E, q);
         __syncthreads();
         if (*E.status) return;
@@ -400,6 +402,7 @@ __device__ __noinline__ void eval_state(EvalCtx &E, const double *q, double tau,
         for (int idx = threadIdx.x; idx < d * d; idx += SGP_NT) H[idx] = 0.0;
         __syncthreads();
         if (lik_on) {
+            SGP_PROF(13);
             if (mp.J == 1)
                 hess_lik_tiled<1>(E, tau, H, d);
             else
@@ -511,13 +514,20 @@ __device__ __noinline__ void eval_trace(EvalCtx &E, const double *q, double tau,
     }
     if (tau != 0.0) {
         if (!E.ext_trace) {
-            build_wpad(mp, W, d, E.wp);
+            {
+                SGP_PROF(10);
+                build_wpad(mp, W, d, E.wp);
+            }
+            SGP_PROF(11);
             if (mp.J == 1)
                 trace_lik_tiled<1>(E, E.wp);
             else
                 trace_lik_tiled<2>(E, E.wp);
         }
-        if (E.ext_trace != 2) project_back(E, tau, F_C0, F_C1, t);
+        if (E.ext_trace != 2) {
+            SGP_PROF(12);
+            project_back(E, tau, F_C0, F_C1, t);
+        }
         for (int a = mp.Dtot + threadIdx.x; a < d; a += SGP_NT) t[a] = 0.0;
     } else {
         for (int a = threadIdx.x; a < d; a += SGP_NT) t[a] = 0.0;

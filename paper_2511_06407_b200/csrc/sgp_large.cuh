@@ -365,6 +365,69 @@ __global__ void k_lg_transpose_block(double *H, int d, int r0, int c0, int nr, i
     }
 }
 
+// dst = src^T (d x d), 32x32 tiles through shared memory (both sides coalesced)
+__global__ void k_lg_transpose(double *dst, const double *src, int d) {
+    __shared__ double t[32][33];
+    const int nt = (d + 31) / 32;
+    for (int tile = blockIdx.x; tile < nt * nt; tile += gridDim.x) {
+        const int by = tile / nt, bx = tile - by * nt;
+        for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+            const int i = by * 32 + r, j = bx * 32 + threadIdx.x;
+            if (i < d && j < d) t[r][threadIdx.x] = src[(size_t)i * d + j];
+        }
+        __syncthreads();
+        for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+            const int i = bx * 32 + r, j = by * 32 + threadIdx.x;
+            if (i < d && j < d) dst[(size_t)i * d + j] = t[threadIdx.x][r];
+        }
+        __syncthreads();
+    }
+}
+
+// Step i of modified Gram-Schmidt on the ROWS of X = Psi^T, i.e. on the
+// columns of Psi as _jacobi.py:90-107 does: column i /= ||column i||, then
+// every column j > i loses its component along column i.  Every block
+// normalises row i into shared memory from the unmodified row; block 0 writes
+// the normalised row i-1 of the previous step (nobody reads it any more), so
+// the steps need no grid-wide barrier.  nrm[0]: norm of row i-1 (0 = skipped).
+__global__ void k_lg_mgs_step(double *X, int d, int i, double *nrm) {
+    extern __shared__ double xi[];
+    __shared__ double red[32];
+    if (blockIdx.x == 0 && i > 0) {
+        const double n0 = nrm[0];
+        __syncthreads();
+        if (n0 != 0.0)
+            for (int k = threadIdx.x; k < d; k += blockDim.x) X[(size_t)(i - 1) * d + k] /= n0;
+    }
+    if (i >= d) return;
+    const double *ri = X + (size_t)i * d;
+    double s = 0.0;
+    for (int k = threadIdx.x; k < d; k += blockDim.x) {
+        const double v = ri[k];
+        xi[k] = v;
+        s += v * v;
+    }
+    s = warp_sum(s);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    double tot = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += red[w];
+    const double n = sqrt(tot);
+    if (blockIdx.x == 0 && threadIdx.x == 0) nrm[0] = n;
+    if (n == 0.0) return;
+    for (int k = threadIdx.x; k < d; k += blockDim.x) xi[k] /= n;
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const int warps = (int)(gridDim.x * (blockDim.x >> 5));
+    for (int j = i + 1 + (int)(blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)); j < d; j += warps) {
+        double *rj = X + (size_t)j * d;
+        double dot = 0.0;
+        for (int k = lane; k < d; k += 32) dot += xi[k] * rj[k];
+        dot = warp_sum(dot);
+        for (int k = lane; k < d; k += 32) rj[k] -= dot * xi[k];
+    }
+}
+
 __global__ void k_lg_mirror_block(double *H, int d, int o, int n) {
     for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < (size_t)n * n;
          idx += (size_t)gridDim.x * blockDim.x) {
@@ -639,12 +702,30 @@ static int lg_eig_cold(LgCtx &c, int dst, int *sweeps) {
     return lg_sync(c);
 }
 
+// Modified Gram-Schmidt of P_slot's columns (_jacobi.py:90-107) as d grid
+// steps on the transposed matrix (rows contiguous); X is free at this point.
+static void lg_mgs(LgCtx &c, int slot) {
+    const int d = c.d;
+    const int nt = (d + 31) / 32;
+    const int tgrid = std::min(nt * nt, 148 * 8);
+    k_lg_transpose<<<tgrid, dim3(32, 8), 0, c.s>>>(c.L.X, c.L.P[slot], d);
+    const size_t smem = (size_t)d * sizeof(double);
+    if (smem > 48 * 1024)
+        cudaFuncSetAttribute(k_lg_mgs_step, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    for (int i = 0; i <= d; ++i) {
+        const int rows = d - 1 - i;
+        const int blocks = std::max(1, std::min((rows + 7) / 8, 148 * 4));
+        k_lg_mgs_step<<<blocks, 256, smem, c.s>>>(c.L.X, d, i, c.L.sc + 12);
+    }
+    k_lg_transpose<<<tgrid, dim3(32, 8), 0, c.s>>>(c.L.P[slot], c.L.X, d);
+}
+
 // warm decomposition of H in P_src's basis into slot dst (metric.py:145-185)
 static int lg_eig_warm(LgCtx &c, int src, int dst, int *sweeps) {
     const int d = c.d;
     int since = c.since[src] + 1;
     if (c.cfg.gs_interval && since >= c.cfg.gs_interval) {
-        lg_op(c, LG_MGS, src);
+        lg_mgs(c, src);
         since = 0;
     }
     const double hnorm = lg_hnorm(c);

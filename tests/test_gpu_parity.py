@@ -175,3 +175,19 @@ def test_oracle_agrees_on_fresh_chain(targets):
                                           record_q=True))
     assert [r.accept for r in res.records] == [r.accept for r in ref.records]
     assert rel_err(res.sample_matrix(), np.vstack([r.q for r in ref.records])) < 1e-9
+
+
+def test_rotation_fast_paths_bit_exact():
+    """The Jacobi's branch-free fp64 div/sqrt/rcp replicas (sgp_core.cuh) equal
+    the library's correctly rounded results bit for bit wherever they report
+    success, on 2^24 Jacobi-like operand triples and raw bit patterns."""
+    import ctypes
+
+    from paper_2511_06407_b200 import _native as nat
+
+    counts = (ctypes.c_longlong * 4)()
+    nat.check(nat.lib().sgp_debug_rotation_check(1 << 24, 2024, counts), "rotation check")
+    bad, slow, badop, n = list(counts)
+    assert n == 1 << 24
+    assert bad == 0 and badop == 0
+    assert slow < n // 100  # the library path is the exception

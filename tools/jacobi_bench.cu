@@ -49,9 +49,13 @@ int main(int argc, char **argv) {
     size_t smem = (64 + 2 * d * d) * 8;
     cudaFuncSetAttribute(bench, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const char *names[] = {"A smem, V smem", "A glob, V smem", "A smem, V glob", "A glob, V glob"};
-    for (int nt : {32, 256}) {
-        for (int mode = 0; mode < 4; ++mode) {
+    // optional argv[2]: one block size only, A and V in shared memory, one CTA (for ncu)
+    const int only = argc > 2 ? atoi(argv[2]) : 0;
+    std::vector<int> nts = only ? std::vector<int>{only} : std::vector<int>{32, 64, 256};
+    for (int nt : nts) {
+        for (int mode = 0; mode < (only ? 1 : 4); ++mode) {
             for (int blocks : {1, 148 * 4}) {
+                if (only && blocks > 1) continue;
                 bench<<<blocks, nt, smem>>>(A0, Ag, Vg, d, mode, cyc, sw);
                 cudaDeviceSynchronize();
                 cudaEvent_t e0, e1;
@@ -68,6 +72,14 @@ int main(int argc, char **argv) {
                 double rot = (double)hs * d * (d - 1) / 2;
                 printf("d=%d nt=%3d %-16s blocks=%4d sweeps=%d  %.0f cyc/rotation  (%.3f ms)\n", d, nt, names[mode],
                        blocks, hs, hc / rot, ms);
+#ifdef SGP_JPROF
+                long long jp[8];
+                cudaMemcpyFromSymbol(jp, sgp_jprof, sizeof(jp));
+                if (jp[3]) printf("   warp0 per iteration: chain %.0f, publish+log %.0f, barrier+operands %.0f cycles (%lld it)\n",
+                                  (double)jp[0] / jp[3], (double)jp[1] / jp[3], (double)jp[2] / jp[3], jp[3]);
+                long long z8[8] = {0};
+                cudaMemcpyToSymbol(sgp_jprof, z8, sizeof(z8));
+#endif
             }
         }
     }

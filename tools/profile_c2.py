@@ -18,6 +18,7 @@ ap.add_argument("--leapfrogs", type=int, default=20)
 ap.add_argument("--order", default="cyclic")
 ap.add_argument("--n", type=int, default=512)
 ap.add_argument("--dims", type=int, default=1)
+ap.add_argument("--config", default=None, help="a tools/bench_configs.py config name prefix, e.g. C3b")
 args = ap.parse_args()
 
 import torch  # noqa: E402
@@ -26,10 +27,20 @@ from paper_2511_06407_b200 import rrgp  # noqa: E402
 from paper_2511_06407_b200.posterior import PosteriorTarget  # noqa: E402
 from paper_2511_06407_b200.sampler import ChainConfig, DeviceChains  # noqa: E402
 
-data, _ = rrgp.simulate_logistic(args.dims, n=args.n, seed=0)
-target = PosteriorTarget(rrgp.build_model("logistic", data.x), data)
+eps = 1e-3
+if args.config:
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    import bench_configs  # noqa: E402
+
+    ccfg = next(c for c in bench_configs.CONFIGS if c["name"].startswith(args.config))
+    model, data = bench_configs.make(ccfg)
+    eps = ccfg["eps"]
+    target = PosteriorTarget(model, data)
+else:
+    data, _ = rrgp.simulate_logistic(args.dims, n=args.n, seed=0)
+    target = PosteriorTarget(rrgp.build_model("logistic", data.x), data)
 d, Z = target.dim, args.chains
-cfg = ChainConfig(epsilon=1e-3, leapfrogs=args.leapfrogs, moves=1, burnin=0, warm_order=args.order)
+cfg = ChainConfig(epsilon=eps, leapfrogs=args.leapfrogs, moves=1, burnin=0, warm_order=args.order)
 ch = DeviceChains(target.device, np.ones(Z), cfg)
 ch.set_q(np.zeros((Z, d)))
 ch.init()
@@ -57,7 +68,8 @@ ch.run(args.moves, z, lu)
 torch.cuda.synchronize()
 L.sgp_debug_phase_cycles(buf, 0)
 names = {0: "W formation", 1: "trace", 2: "state+Hessian", 3: "MGS", 4: "PsiT H Psi", 5: "warm Jacobi",
-         8: "cold Jacobi", 9: "leapfrog total"}
+         8: "cold Jacobi", 10: " trace: build Wp", 11: " trace: per-sample forms", 12: " trace: project", 13: " Hessian lik block",
+         14: " state: f + derivatives", 9: "leapfrog total"}
 tot = buf[9] or 1
 nlf = args.moves * args.leapfrogs
 for k, nm in names.items():
