@@ -841,7 +841,13 @@ extern "C" int sgp_run_moves(const sgp_model *m, const sgp_chain_config *cfg, co
     if (L.nt == 32) {
         SGP_LAUNCH_MOVES(32, 12);
     } else if (L.nt == 64) {
-        SGP_LAUNCH_MOVES(64, 6);
+        if (L.per_sm >= 10) {
+            SGP_LAUNCH_MOVES(64, 10);
+        } else if (L.per_sm >= 8) {
+            SGP_LAUNCH_MOVES(64, 8);
+        } else {
+            SGP_LAUNCH_MOVES(64, 6);
+        }
     } else if (L.nt == 128) {
         SGP_LAUNCH_MOVES(128, 4);
     } else {

@@ -32,7 +32,7 @@ struct SmemPlan {
 __host__ __device__ inline size_t sgp_round2(size_t x) { return (x + 1) & ~size_t(1); }
 
 __host__ __device__ inline size_t sgp_stage_doubles(int Dp, int CH) {
-    return sgp_round2(2 * ((size_t)CH * (Dp + 2) + 3 * (size_t)CH) + (size_t)(Dp / 4) * CH * 3 + 2);
+    return sgp_round2(2 * ((size_t)CH * (Dp + 2) + 3 * (size_t)CH) + 2 * (size_t)(Dp / 4) * CH * 3 + 2);
 }
 
 __host__ __device__ inline size_t sgp_mat_doubles(int i, int d, int Dp) {
@@ -99,6 +99,23 @@ __device__ inline void setup_ws(ChainWS &w, EvalCtx &E, char *smem, const SmemPl
     __syncthreads();
 }
 
+// Working copy of the eigenvector matrix during a cyclic Jacobi, stored
+// column-major so the row-parallel log application is coalesced (global) /
+// conflict-free (shared): the tile stage when it fits (idle during the
+// Jacobi), else the X scratch matrix (free between Psi^T H Psi and the next W).
+__device__ __forceinline__ double *jac_vwork(const ChainWS &w, const EvalCtx &E, int d) {
+    if (E.stage && (size_t)d * d <= sgp_stage_doubles(E.M.mp.Dp, E.CH)) return E.stage;
+    return w.X;
+}
+// Vt (column-major) -> P (row-major)
+__device__ __forceinline__ void jac_vwork_out(double *P, const double *Vt, int d) {
+    for (int idx = threadIdx.x; idx < d * d; idx += SGP_NT) {
+        const int j = idx / d, k = idx - j * d;
+        P[k * d + j] = Vt[idx];
+    }
+    __syncthreads();
+}
+
 // ---------------------------------------------------------------------------
 // eigendecompositions into ping-pong slot `dst`
 
@@ -108,12 +125,18 @@ __device__ __noinline__ int eig_cold(ChainWS &w, EvalCtx &E, int d, const sgp_ch
     const double hnorm = sqrt(frob2(w.H, d * d, E.red));
     const double tol = cfg.zeta * hnorm;
     const double skip = d ? tol / d : 0.0;
-    mat_identity(w.P[dst], d);
+    double *Vt = jac_vwork(w, E, d);
+    for (int idx = threadIdx.x; idx < d * d; idx += SGP_NT) {
+        const int j = idx / d, k = idx - j * d;
+        Vt[idx] = k == j ? 1.0 : 0.0;
+    }
+    __syncthreads();
     int sw;
     {
         SGP_PROF(8);
-        sw = jacobi_cyclic(w.H, w.P[dst], d, tol, skip, cfg.sweep_cap, E.red, w.jlog);
+        sw = jacobi_cyclic(w.H, Vt, d, tol, skip, cfg.sweep_cap, E.red, w.jlog, 1, d);
     }
+    jac_vwork_out(w.P[dst], Vt, d);
     if (sweeps_out) *sweeps_out = sw;
     if (sw < 0) return SGP_STATUS_JACOBI;
     for (int j = threadIdx.x; j < d; j += SGP_NT) w.lam[dst][j] = w.H[j * d + j];
@@ -143,16 +166,25 @@ __device__ __noinline__ int eig_warm(ChainWS &w, EvalCtx &E, int d, const sgp_ch
         mat_mul<2>(w.X, w.P[src], w.H, d);  // X = Psi^T H
         mat_mul<0>(w.H, w.X, w.P[src], d);  // A = X Psi
         mat_symmetrize(w.H, d);
-        mat_copy(w.P[dst], w.P[src], d * d);  // rotations applied to Psi directly (== Psi Q)
     }
     const double tol = cfg.zeta * hnorm;
     const double skip = d ? tol / d : 0.0;
     int sw;
     SGP_PROF(5);
-    if (cfg.warm_order == SGP_ORDER_CYCLIC)
-        sw = jacobi_cyclic(w.H, w.P[dst], d, tol, skip, cfg.sweep_cap, E.red, w.jlog);
-    else
+    if (cfg.warm_order == SGP_ORDER_CYCLIC) {
+        // rotations applied to Psi directly (== Psi Q), in shared memory when it fits
+        double *Vt = jac_vwork(w, E, d);
+        for (int idx = threadIdx.x; idx < d * d; idx += SGP_NT) {
+            const int j = idx / d, k = idx - j * d;
+            Vt[idx] = w.P[src][k * d + j];
+        }
+        __syncthreads();
+        sw = jacobi_cyclic(w.H, Vt, d, tol, skip, cfg.sweep_cap, E.red, w.jlog, 1, d);
+        jac_vwork_out(w.P[dst], Vt, d);
+    } else {
+        mat_copy(w.P[dst], w.P[src], d * d);
         sw = jacobi_parallel(w.H, w.P[dst], d, tol, skip, cfg.sweep_cap, E.red, w.prm);
+    }
     if (sweeps_out) *sweeps_out = sw;
     if (sw < 0) return SGP_STATUS_JACOBI;
     for (int j = threadIdx.x; j < d; j += SGP_NT) w.lam[dst][j] = w.H[j * d + j];

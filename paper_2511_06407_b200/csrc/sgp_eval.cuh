@@ -140,7 +140,20 @@ __device__ __noinline__ void hess_lik_tiled(EvalCtx &E, double tau, double *H, i
     const ModelParams &mp = E.M.mp;
     const int CH = E.CH, SP = mp.Dp + 2, nb = mp.Dp >> 2, ld = mp.ld;
     const int ntile = nb * (nb + 1) / 2;
-    const int R = max(1, min(8, SGP_NT / max(1, ntile)));
+    // sample replicas per tile: the R in 1..8 with the fewest rounds per sample
+    int R = 1;
+    {
+        double best = 1e30;
+        for (int r = 1; r <= 8; ++r) {
+            // rounds per thread x samples per round, plus one Phi staging pass per 2*NT items
+            const double cost = (double)((ntile * r + SGP_NT - 1) / SGP_NT) / r +
+                                0.25 * ((ntile * r + 2 * SGP_NT - 1) / (2 * SGP_NT)) + 0.02 * r;
+            if (cost < best) {
+                best = cost;
+                R = r;
+            }
+        }
+    }
     const int items = ntile * R;
     for (int base = 0; base < items; base += 2 * SGP_NT) {
         int a0[2], b0[2], rep[2], nmine = 0;
@@ -236,7 +249,10 @@ __device__ __noinline__ void trace_lik_tiled(EvalCtx &E, const double *Wp) {
     const ModelParams &mp = E.M.mp;
     const int CH = E.CH, SP = mp.Dp + 2, Dp = mp.Dp, nb = Dp >> 2, ld = mp.ld;
     const int ngrp = CH >> 2, tiles = ngrp * nb;
-    double *part = stage_buf(E, 2);  // nb * CH * 3, after the two stage buffers
+    // K split: with fewer tiles than threads, ks threads share a tile, each
+    // over a slice of the contraction index; their row-dot partials add.
+    const int ks = (2 * tiles <= SGP_NT) ? 2 : 1;
+    double *part = stage_buf(E, 2);  // ks * nb * CH * 3, after the two stage buffers
     __syncthreads();
     stage_issue(E, 0, 0, 0, 0);
     for (int k = 0, i0 = 0; i0 < mp.N; ++k, i0 += CH) {
@@ -248,13 +264,15 @@ __device__ __noinline__ void trace_lik_tiled(EvalCtx &E, const double *Wp) {
         }
         __syncthreads();
         const double *stg = stage_buf(E, k & 1);
-        for (int t = threadIdx.x; t < tiles; t += SGP_NT) {
+        for (int it = threadIdx.x; it < tiles * ks; it += SGP_NT) {
+            const int h = it / tiles, t = it - h * tiles;
             const int g = t / nb, bt = t - g * nb;
             const int ii0 = 4 * g, b0 = 4 * bt;
             double y0[16], y1[16];
 #pragma unroll
             for (int e = 0; e < 16; ++e) y0[e] = y1[e] = 0.0;
-            for (int a = 0; a < mp.Dp0; ++a) {
+            const int a0lo = (mp.Dp0 * h) / ks, a0hi = (mp.Dp0 * (h + 1)) / ks;
+            for (int a = a0lo; a < a0hi; ++a) {
                 double w[4];
                 load4(Wp + a * Dp + b0, w);
 #pragma unroll
@@ -265,7 +283,9 @@ __device__ __noinline__ void trace_lik_tiled(EvalCtx &E, const double *Wp) {
                 }
             }
             if (J == 2) {
-                for (int a = mp.Dp0; a < Dp; ++a) {
+                const int D1 = Dp - mp.Dp0;
+                const int a1lo = mp.Dp0 + (D1 * h) / ks, a1hi = mp.Dp0 + (D1 * (h + 1)) / ks;
+                for (int a = a1lo; a < a1hi; ++a) {
                     double w[4];
                     load4(Wp + a * Dp + b0, w);
 #pragma unroll
@@ -287,7 +307,7 @@ __device__ __noinline__ void trace_lik_tiled(EvalCtx &E, const double *Wp) {
                     p0 += y0[u * 4 + v] * xb[v];
                     p1 += y1[u * 4 + v] * xb[v];
                 }
-                double *pp = part + ((size_t)bt * CH + ii0 + u) * 3;
+                double *pp = part + (((size_t)h * nb + bt) * CH + ii0 + u) * 3;
                 pp[0] = jb ? 0.0 : p0;
                 pp[1] = jb ? p0 : p1;
                 pp[2] = jb ? p1 : 0.0;
@@ -298,7 +318,7 @@ __device__ __noinline__ void trace_lik_tiled(EvalCtx &E, const double *Wp) {
             const int i = i0 + ii;
             if (i >= mp.N) continue;
             double s00 = 0.0, sx = 0.0, s11 = 0.0;
-            for (int bt = 0; bt < nb; ++bt) {
+            for (int bt = 0; bt < nb * ks; ++bt) {
                 const double *pp = part + ((size_t)bt * CH + ii) * 3;
                 s00 += pp[0];
                 sx += pp[1];

@@ -4,6 +4,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
+#include <algorithm>
 
 #include "../paper_2511_06407_b200/csrc/sgp_core.cuh"
 
@@ -11,7 +12,7 @@ __global__ void bench(const double *A0, double *Ag, double *Vg, int d, int mode,
     extern __shared__ double sm[];
     double *red = sm;
     double *As = sm + 64;
-    double *Vs = As + d * d;
+    double *Vs = (mode & 1) ? As : As + d * d;
     double *A = (mode & 1) ? Ag + blockIdx.x * d * d : As;
     double *V = (mode & 2) ? Vg + blockIdx.x * d * d : Vs;
     for (int i = threadIdx.x; i < d * d; i += blockDim.x) {
@@ -46,16 +47,18 @@ int main(int argc, char **argv) {
     cudaMalloc(&cyc, 8);
     cudaMalloc(&sw, 4);
     cudaMemcpy(A0, a.data(), d * d * 8, cudaMemcpyHostToDevice);
-    size_t smem = (64 + 2 * d * d) * 8;
-    cudaFuncSetAttribute(bench, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    size_t smem_full = (64 + 2 * d * d) * 8;
+    cudaFuncSetAttribute(bench, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::min<size_t>(smem_full, 227 * 1024));
     const char *names[] = {"A smem, V smem", "A glob, V smem", "A smem, V glob", "A glob, V glob"};
     // optional argv[2]: one block size only, A and V in shared memory, one CTA (for ncu)
     const int only = argc > 2 ? atoi(argv[2]) : 0;
+    const int only_mode = argc > 3 ? atoi(argv[3]) : 0;
     std::vector<int> nts = only ? std::vector<int>{only} : std::vector<int>{32, 64, 256};
     for (int nt : nts) {
-        for (int mode = 0; mode < (only ? 1 : 4); ++mode) {
-            for (int blocks : {1, 148 * 4}) {
-                if (only && blocks > 1) continue;
+        for (int mode = only ? only_mode : 0; mode < (only ? only_mode + 1 : 4); ++mode) {
+            const size_t smem = (64 + ((mode & 1) ? 0 : d * d) + ((mode & 2) ? 0 : d * d)) * 8;
+            if (smem > 227 * 1024) continue;
+            for (int blocks : {1, 148}) {
                 bench<<<blocks, nt, smem>>>(A0, Ag, Vg, d, mode, cyc, sw);
                 cudaDeviceSynchronize();
                 cudaEvent_t e0, e1;
@@ -75,8 +78,9 @@ int main(int argc, char **argv) {
 #ifdef SGP_JPROF
                 long long jp[8];
                 cudaMemcpyFromSymbol(jp, sgp_jprof, sizeof(jp));
-                if (jp[3]) printf("   warp0 per iteration: chain %.0f, publish+log %.0f, barrier+operands %.0f cycles (%lld it)\n",
-                                  (double)jp[0] / jp[3], (double)jp[1] / jp[3], (double)jp[2] / jp[3], jp[3]);
+                if (jp[3]) printf("   warp0 per iteration: barrier %.0f, chain %.0f, tail %.0f cycles; %lld it, %lld rotated; sweep total %.0f per it\n",
+                                  (double)jp[0] / jp[3], (double)jp[1] / jp[3], (double)jp[2] / jp[3], jp[3], jp[4], (double)jp[5] / jp[3]);
+                if (jp[3]) printf("   row start barrier %.0f, row end barrier %.0f cycles per iteration\n", (double)jp[6] / jp[3], (double)jp[7] / jp[3]);
                 long long z8[8] = {0};
                 cudaMemcpyToSymbol(sgp_jprof, z8, sizeof(z8));
 #endif
