@@ -19,8 +19,8 @@ struct ChainWS {
 
 // Shared-memory layout (host and device compute it identically).
 // Matrices, in placement priority: H (the serial Jacobi works in it every
-// rotation), Wp (padded contraction matrix read by every trace tile), W, P0,
-// P1, X, T.  Those that do not fit the per-CTA budget live in the chain's
+// rotation), Wp (padded contraction matrix read by every trace tile; aliases
+// H when H is placed), W, P0, P1, X (aliases the tile stage when it fits), T.  Those that do not fit the per-CTA budget live in the chain's
 // L2-resident scratch slice, so several chains can share an SM.
 #define SGP_NMAT 7
 struct SmemPlan {
@@ -52,6 +52,19 @@ __host__ __device__ inline SmemPlan sgp_smem_plan(int d, int Dp, int nt, size_t 
     off += sgp_stage_doubles(Dp, s.CH) * sizeof(double);
     for (int i = 0; i < SGP_NMAT; ++i) {
         const size_t m = sgp_round2(sgp_mat_doubles(i, d, Dp)) * sizeof(double);
+        // Wp (padded trace operand) shares H's slot: H is consumed by the
+        // eigendecomposition right after every Hessian evaluation and Wp
+        // lives only inside one trace contraction
+        if (i == 1 && s.off_mat[0] != (size_t)-1 && (size_t)Dp * Dp <= (size_t)d * d) {
+            s.off_mat[1] = s.off_mat[0];
+            continue;
+        }
+        // X (product scratch of the W formation and Psi^T H Psi) shares the
+        // tile stage, which is idle in both
+        if (i == 5 && (size_t)d * d <= sgp_stage_doubles(Dp, s.CH)) {
+            s.off_mat[5] = s.off_stage;
+            continue;
+        }
         if (off + m <= budget) {
             s.off_mat[i] = off;
             off += m;
