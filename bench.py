@@ -391,6 +391,16 @@ def run_gpu(args):
             line["min_ess"] = ess
         if os.path.exists(peaks_path):
             line["roofline"]["peaks_file"] = "MEASURED_PEAKS.json present (bf16/HBM only)"
+        # DRAM bytes per launch of this kernel from the committed ncu --set full capture
+        # of the same command (profiles/), when it was taken on this configuration
+        tpath = os.path.join(ROOT, "profiles", "r1_traffic_k_run_moves.json")
+        if os.path.exists(tpath):
+            with open(tpath) as f:
+                tr = json.load(f)
+            if tr.get("chains") == Z and tr.get("leapfrogs") == LEAPFROGS:
+                line["roofline"]["traffic"] = tr["dram_bytes_per_launch"]
+                line["roofline"]["traffic_unit"] = "bytes/launch (DRAM read+write, ncu)"
+                line["roofline"]["traffic_source"] = "profiles/r1_traffic_k_run_moves.json"
         if world == 1 and not args.no_cpu_baseline:
             cores = os.cpu_count() or 1
             pool = CpuPool(cores)
@@ -417,8 +427,8 @@ def main():
     ap.add_argument("--warm-order", default="cyclic", choices=["cyclic", "parallel"])
     ap.add_argument("--ref-leapfrogs", type=int, default=20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--ess-moves", type=int, default=120, help="recorded moves of the min-ESS pilot (0: skip)")
-    ap.add_argument("--ess-burnin", type=int, default=30)
+    ap.add_argument("--ess-moves", type=int, default=300, help="recorded moves of the min-ESS pilot (0: skip)")
+    ap.add_argument("--ess-burnin", type=int, default=100)
     ap.add_argument("--ess-chains-per-sm", type=int, default=2)
     args = ap.parse_args()
     if args.impl == "reference":

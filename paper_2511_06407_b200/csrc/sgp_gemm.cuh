@@ -37,6 +37,10 @@ struct GemmArgs {
     double alpha, beta;
     int upper_only;  // only tiles with m-tile <= n-tile (symmetric outputs, mirrored later)
     int a16, b16;    // operand rows 16-byte aligned (set by gemm_launch); else 8-byte copies
+    // K-split gather (block-Jacobi updates): for k >= ksplit the operand with a
+    // non-null second base reads A2 / B2 at k - ksplit.  ksplit % GM_BK == 0.
+    const double *A2, *B2;
+    int ksplit;
 };
 
 __device__ __forceinline__ void dmma_m8n8k4(double &c0, double &c1, double a, double b) {
@@ -71,6 +75,10 @@ __device__ __forceinline__ void gm_issue(const GemmArgs &g, double *st, int m0, 
     using T = GmTile<TA, TB>;
     const int tid = threadIdx.x;
     double *As = st, *Bs = st + T::A_SZ, *Ss = st + T::A_SZ + T::B_SZ;
+    // operand bases and k offsets of this k-tile (K-split gather)
+    const bool sa = g.A2 && g.ksplit && k0 >= g.ksplit, sb = g.B2 && g.ksplit && k0 >= g.ksplit;
+    const double *Ab = sa ? g.A2 : g.A, *Bb = sb ? g.B2 : g.B;
+    const int dka = sa ? -g.ksplit : 0, dkb = sb ? -g.ksplit : 0;
     // A: rows of A_COLS doubles, A_COLS/2 16-byte chunks per row
     constexpr int ACH = T::A_COLS / 2, BCH = T::B_COLS / 2;
     if (!g.a16) {
@@ -78,7 +86,8 @@ __device__ __forceinline__ void gm_issue(const GemmArgs &g, double *st, int m0, 
             const int r = e / T::A_COLS, c = e - r * T::A_COLS;
             const int gr = (TA ? k0 : m0) + r, gc = (TA ? m0 : k0) + c;
             const bool ok = gr < (TA ? g.K : g.M) && gc < (TA ? g.M : g.K);
-            gm_cp8(As + r * T::A_LD + c, g.A + (ok ? (size_t)gr * g.lda + gc : 0), ok);
+            const int ar = gr + (TA ? dka : 0), ac = gc + (TA ? 0 : dka);
+            gm_cp8(As + r * T::A_LD + c, Ab + (ok ? (size_t)ar * g.lda + ac : 0), ok);
         }
     } else {
 #pragma unroll
@@ -88,7 +97,8 @@ __device__ __forceinline__ void gm_issue(const GemmArgs &g, double *st, int m0, 
         const int rlim = TA ? g.K : g.M, clim = TA ? g.M : g.K;
         const bool ok = gr < rlim && gc < clim;
         // the pair (gc, gc+1): when gc+1 is past the edge the row tail is zero-filled by a 8-byte copy
-        const double *src = g.A + (size_t)(ok ? gr : 0) * g.lda + (ok ? gc : 0);
+        const int ar = gr + (TA ? dka : 0), ac = gc + (TA ? 0 : dka);
+        const double *src = Ab + (size_t)(ok ? ar : 0) * g.lda + (ok ? ac : 0);
         if (ok && gc + 1 >= clim) {
             gm_cp8(As + r * T::A_LD + c, src, true);
             gm_cp8(As + r * T::A_LD + c + 1, src, false);
@@ -102,7 +112,8 @@ __device__ __forceinline__ void gm_issue(const GemmArgs &g, double *st, int m0, 
             const int r = e / T::B_COLS, c = e - r * T::B_COLS;
             const int gr = (TB ? n0 : k0) + r, gc = (TB ? k0 : n0) + c;
             const bool ok = gr < (TB ? g.N : g.K) && gc < (TB ? g.K : g.N);
-            gm_cp8(Bs + r * T::B_LD + c, g.B + (ok ? (size_t)gr * g.ldb + gc : 0), ok);
+            const int br = gr + (TB ? 0 : dkb), bc = gc + (TB ? dkb : 0);
+            gm_cp8(Bs + r * T::B_LD + c, Bb + (ok ? (size_t)br * g.ldb + bc : 0), ok);
         }
     } else
 #pragma unroll
@@ -111,7 +122,8 @@ __device__ __forceinline__ void gm_issue(const GemmArgs &g, double *st, int m0, 
         const int gr = (TB ? n0 : k0) + r, gc = (TB ? k0 : n0) + c;
         const int rlim = TB ? g.N : g.K, clim = TB ? g.K : g.N;
         const bool ok = gr < rlim && gc < clim;
-        const double *src = g.B + (size_t)(ok ? gr : 0) * g.ldb + (ok ? gc : 0);
+        const int br = gr + (TB ? 0 : dkb), bc = gc + (TB ? dkb : 0);
+        const double *src = Bb + (size_t)(ok ? br : 0) * g.ldb + (ok ? bc : 0);
         if (ok && gc + 1 >= clim) {
             gm_cp8(Bs + r * T::B_LD + c, src, true);
             gm_cp8(Bs + r * T::B_LD + c + 1, src, false);
@@ -133,10 +145,11 @@ __device__ __forceinline__ void gm_issue(const GemmArgs &g, double *st, int m0, 
 }
 
 template <int TA, int TB>
-__global__ void __launch_bounds__(GM_THREADS) k_gemm_dmma(GemmArgs g) {
+__device__ __forceinline__ void gm_body(const GemmArgs &g) {
     using T = GmTile<TA, TB>;
     const int tm = blockIdx.y, tn = blockIdx.x;
     if (g.upper_only && tm > tn) return;
+    if (tm * GM_BM >= g.M || tn * GM_BN >= g.N) return;  // batched launches size the grid for the largest
     extern __shared__ __align__(16) double gsm[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
@@ -208,6 +221,18 @@ __global__ void __launch_bounds__(GM_THREADS) k_gemm_dmma(GemmArgs g) {
     }
 }
 
+template <int TA, int TB>
+__global__ void __launch_bounds__(GM_THREADS) k_gemm_dmma(GemmArgs g) {
+    gm_body<TA, TB>(g);
+}
+
+// one GEMM per blockIdx.z (independent outputs); grid sized for the largest
+template <int TA, int TB>
+__global__ void __launch_bounds__(GM_THREADS) k_gemm_dmma_batched(const GemmArgs *gs) {
+    const GemmArgs g = gs[blockIdx.z];
+    gm_body<TA, TB>(g);
+}
+
 // mirror the upper triangle of an n x n matrix into the lower one
 __global__ void k_mirror_upper(double *C, int n, int ldc) {
     for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < (size_t)n * n;
@@ -238,4 +263,21 @@ static inline cudaError_t gemm_launch(GemmArgs g, cudaStream_t s) {
     if (g.TA)
         return g.TB ? gemm_launch_t<1, 1>(g, s) : gemm_launch_t<1, 0>(g, s);
     return g.TB ? gemm_launch_t<0, 1>(g, s) : gemm_launch_t<0, 0>(g, s);
+}
+
+// Batched launch: nb descriptors in device memory (all with the same TA, TB
+// and alignment flags, set by the caller); grid covers max M x max N.
+template <int TA, int TB>
+static inline cudaError_t gemm_launch_batched(const GemmArgs *d_gs, int nb, int maxM, int maxN, cudaStream_t s) {
+    using T = GmTile<TA, TB>;
+    static bool configured = false;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(k_gemm_dmma_batched<TA, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)T::SMEM);
+        if (e != cudaSuccess) return e;
+        configured = true;
+    }
+    dim3 grid((maxN + GM_BN - 1) / GM_BN, (maxM + GM_BM - 1) / GM_BM, nb);
+    k_gemm_dmma_batched<TA, TB><<<grid, GM_THREADS, T::SMEM, s>>>(d_gs);
+    return cudaGetLastError();
 }
