@@ -24,6 +24,12 @@ struct LgPtrs {
     ModelDev M;
     double *S, *H, *X, *W, *P[2], *Y, *sacc, *vec, *sc, *jlog, *jprm, *red;
     int *si, *status, *jpairs;
+    // block Jacobi (round-robin order, warm and cold decompositions at large d)
+    int bj_dp, bj_nbk;           // padded dimension (multiple of 2*BJ_B), number of blocks (even)
+    double *bjA, *bjT, *bjV[2];  // bj_dp x bj_dp working matrices
+    double *bjU, *bjLam, *bjPart;
+    int *bjCnt;
+    GemmArgs *bjDesc;            // [round][col A | row A | col V even | col V odd][2 * pairs]
 };
 
 struct LargeWS {
@@ -517,6 +523,240 @@ __global__ void k_lg_project(LgPtrs L, double tau, int field0, int field1, doubl
 }
 
 // ---------------------------------------------------------------------------
+// Block Jacobi for large d (round-robin pair order: warm
+// decompositions are order-insensitive to the Jacobi tolerance).  The padded
+// matrix is split into blocks of BJ_B; each round pairs the blocks
+// round-robin, every pair's 2*BJ_B x 2*BJ_B subproblem [A_II A_IJ; A_JI A_JJ]
+// is diagonalised in shared memory by the same rotation formula, skip rule
+// and (per inner sweep) convergence rule as the reference, and the pair
+// transformations U are applied to A (columns, then rows) and to V as
+// batched FP64 tensor-core GEMMs (DMMA, K gathered from the two blocks).
+// Convergence: off-norm(A) <= tol before each outer sweep (_jacobi.py:50-51).
+#define BJ_B 32
+#define BJ_N (2 * BJ_B)
+#define BJ_INNER_CAP 60
+#define BJ_SMEM ((size_t)2 * BJ_N * (BJ_N + 1) * sizeof(double))
+
+__host__ __device__ inline void bj_pair(int r, int k, int nbk, int &I, int &J) {
+    int a, b;
+    if (k == 0) {
+        a = r;
+        b = nbk - 1;
+    } else {
+        a = (r + k) % (nbk - 1);
+        b = (r - k + nbk - 1) % (nbk - 1);
+    }
+    I = a < b ? a : b;
+    J = a < b ? b : a;
+}
+
+__global__ void __launch_bounds__(256) k_bj_solve(const double *A, int dp, int r, int nbk, double skip, double *Uall,
+                                                  double *lamall, int *cnt) {
+    extern __shared__ double bjsm[];  // S and U, rows padded to BJ_N + 1
+    double(*S)[BJ_N + 1] = reinterpret_cast<double(*)[BJ_N + 1]>(bjsm);
+    double(*U)[BJ_N + 1] = reinterpret_cast<double(*)[BJ_N + 1]>(bjsm + BJ_N * (BJ_N + 1));
+    __shared__ double rc[BJ_N / 2], rs[BJ_N / 2], rt[BJ_N / 2], rpp[BJ_N / 2], rqq[BJ_N / 2];
+    __shared__ int rp[BJ_N / 2], rq[BJ_N / 2], ract[BJ_N / 2];
+    __shared__ int any, nrot;
+    const int k = blockIdx.x, tid = threadIdx.x;
+    int I, J;
+    bj_pair(r, k, nbk, I, J);
+    for (int idx = tid; idx < BJ_N * BJ_N; idx += blockDim.x) {
+        const int i = idx / BJ_N, j = idx - i * BJ_N;
+        const int gi = i < BJ_B ? I * BJ_B + i : J * BJ_B + i - BJ_B;
+        const int gj = j < BJ_B ? I * BJ_B + j : J * BJ_B + j - BJ_B;
+        S[i][j] = A[(size_t)gi * dp + gj];
+        U[i][j] = i == j ? 1.0 : 0.0;
+    }
+    if (tid == 0) nrot = 0;
+    __syncthreads();
+    constexpr int m = BJ_N, np = BJ_N / 2;
+    for (int sweep = 0; sweep < BJ_INNER_CAP; ++sweep) {
+        if (tid == 0) any = 0;
+        __syncthreads();
+        for (int rr = 0; rr < m - 1; ++rr) {
+            if (tid < np) {
+                int a, b;
+                if (tid == 0) {
+                    a = rr;
+                    b = m - 1;
+                } else {
+                    a = (rr + tid) % (m - 1);
+                    b = (rr - tid + m - 1) % (m - 1);
+                }
+                const int p = min(a, b), q = max(a, b);
+                const double apq = S[p][q];
+                const bool act = fabs(apq) > skip;
+                double c = 1.0, sn = 0.0, t = 0.0;
+                const double app = S[p][p], aqq = S[q][q];
+                if (act) jacobi_rot(app, aqq, apq, c, sn, t);
+                rc[tid] = c;
+                rs[tid] = sn;
+                rt[tid] = t * apq;
+                rpp[tid] = app;
+                rqq[tid] = aqq;
+                rp[tid] = p;
+                rq[tid] = q;
+                ract[tid] = act;
+                if (act) {
+                    any = 1;
+                    atomicAdd(&nrot, 1);
+                }
+            }
+            __syncthreads();
+            // rows p, q
+            for (int it = tid; it < np * m; it += blockDim.x) {
+                const int kk = it / m, l = it - kk * m;
+                if (!ract[kk]) continue;
+                const int p = rp[kk], q = rq[kk];
+                const double c = rc[kk], sn = rs[kk];
+                const double ap = S[p][l], aq = S[q][l];
+                S[p][l] = c * ap - sn * aq;
+                S[q][l] = sn * ap + c * aq;
+            }
+            __syncthreads();
+            // columns p, q of S and U
+            for (int it = tid; it < np * m; it += blockDim.x) {
+                const int l = it / np, kk = it - l * np;
+                if (!ract[kk]) continue;
+                const int p = rp[kk], q = rq[kk];
+                const double c = rc[kk], sn = rs[kk];
+                const double ap = S[l][p], aq = S[l][q];
+                S[l][p] = c * ap - sn * aq;
+                S[l][q] = sn * ap + c * aq;
+                const double up = U[l][p], uq = U[l][q];
+                U[l][p] = c * up - sn * uq;
+                U[l][q] = sn * up + c * uq;
+            }
+            __syncthreads();
+            if (tid < np && ract[tid]) {
+                const int p = rp[tid], q = rq[tid];
+                S[p][q] = 0.0;
+                S[q][p] = 0.0;
+                S[p][p] = rpp[tid] - rt[tid];
+                S[q][q] = rqq[tid] + rt[tid];
+            }
+            __syncthreads();
+        }
+        if (!any) break;
+    }
+    double *Uk = Uall + (size_t)k * BJ_N * BJ_N;
+    for (int idx = tid; idx < BJ_N * BJ_N; idx += blockDim.x) Uk[idx] = U[idx / BJ_N][idx % BJ_N];
+    for (int i = tid; i < BJ_N; i += blockDim.x) lamall[(size_t)k * BJ_N + i] = S[i][i];
+    if (tid == 0) cnt[k] = nrot;
+}
+
+// exact diagonal blocks of every pair after its transformation: diag(lambda), zeros
+__global__ void k_bj_fix(double *A, int dp, int r, int nbk, const double *lamall, const int *cnt) {
+    const int k = blockIdx.x;
+    if (!cnt[k]) return;
+    int I, J;
+    bj_pair(r, k, nbk, I, J);
+    for (int idx = threadIdx.x; idx < BJ_N * BJ_N; idx += blockDim.x) {
+        const int i = idx / BJ_N, j = idx - i * BJ_N;
+        const int gi = i < BJ_B ? I * BJ_B + i : J * BJ_B + i - BJ_B;
+        const int gj = j < BJ_B ? I * BJ_B + j : J * BJ_B + j - BJ_B;
+        A[(size_t)gi * dp + gj] = i == j ? lamall[(size_t)k * BJ_N + i] : 0.0;
+    }
+}
+
+// off-diagonal sum of squares, deterministic: per-block partials then one ordered sum
+__global__ void k_bj_offnorm(const double *A, int dp, double *part) {
+    __shared__ double red[32];
+    double s = 0.0;
+    for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < (size_t)dp * dp;
+         idx += (size_t)gridDim.x * blockDim.x) {
+        const size_t i = idx / dp, j = idx - i * dp;
+        if (i != j) s += A[idx] * A[idx];
+    }
+    s = warp_sum(s);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+        part[blockIdx.x] = t;
+    }
+}
+__global__ void k_bj_offnorm_final(const double *part, int n, double *out) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        double t = 0.0;
+        for (int i = 0; i < n; ++i) t += part[i];
+        *out = sqrt(t);
+    }
+}
+
+// padded working copies in / results out
+__global__ void k_bj_in(double *Ap, double *Vp, const double *H, const double *P, int d, int dp, int identity) {
+    for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < (size_t)dp * dp;
+         idx += (size_t)gridDim.x * blockDim.x) {
+        const int i = (int)(idx / dp), j = (int)(idx - (size_t)i * dp);
+        const bool in = i < d && j < d;
+        Ap[idx] = in ? H[(size_t)i * d + j] : 0.0;
+        Vp[idx] = in ? (identity ? (i == j ? 1.0 : 0.0) : P[(size_t)i * d + j]) : (i == j ? 1.0 : 0.0);
+    }
+}
+__global__ void k_bj_out(double *H, double *P, const double *Ap, const double *Vp, int d, int dp) {
+    for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < (size_t)d * d;
+         idx += (size_t)gridDim.x * blockDim.x) {
+        const int i = (int)(idx / d), j = (int)(idx - (size_t)i * d);
+        P[idx] = Vp[(size_t)i * dp + j];
+        if (i == j) H[idx] = Ap[(size_t)i * dp + j];
+    }
+}
+
+// Descriptors of the three batched update GEMMs of every round (host side).
+static void bj_build_desc(const LgPtrs &L, std::vector<GemmArgs> &out) {
+    const int dp = L.bj_dp, nbk = L.bj_nbk, np = nbk / 2;
+    out.clear();
+    for (int r = 0; r < nbk - 1; ++r) {
+        for (int kind = 0; kind < 4; ++kind) {  // 0 col A, 1 row A, 2 col V (V0->V1), 3 col V (V1->V0)
+            for (int k = 0; k < np; ++k) {
+                int I, J;
+                bj_pair(r, k, nbk, I, J);
+                const double *Uk = L.bjU + (size_t)k * BJ_N * BJ_N;
+                for (int h = 0; h < 2; ++h) {
+                    const int O = h ? J : I;
+                    GemmArgs g{};
+                    g.alpha = 1.0;
+                    g.beta = 0.0;
+                    g.K = BJ_N;
+                    g.ksplit = BJ_B;
+                    if (kind == 1) {
+                        // A[O rows, :] = U[:, h]^T T[I|J rows, :]
+                        g.M = BJ_B;
+                        g.N = dp;
+                        g.A = Uk + h * BJ_B;
+                        g.lda = BJ_N;
+                        g.TA = 1;
+                        g.B = L.bjT + (size_t)I * BJ_B * dp;
+                        g.B2 = L.bjT + (size_t)J * BJ_B * dp;
+                        g.ldb = dp;
+                        g.C = L.bjA + (size_t)O * BJ_B * dp;
+                    } else {
+                        // X[:, O cols] = Y[:, I|J cols] U[:, h]
+                        const double *Y = kind == 0 ? L.bjA : (kind == 2 ? L.bjV[0] : L.bjV[1]);
+                        double *X = kind == 0 ? L.bjT : (kind == 2 ? L.bjV[1] : L.bjV[0]);
+                        g.M = dp;
+                        g.N = BJ_B;
+                        g.A = Y + (size_t)I * BJ_B;
+                        g.A2 = Y + (size_t)J * BJ_B;
+                        g.lda = dp;
+                        g.B = Uk + h * BJ_B;
+                        g.ldb = BJ_N;
+                        g.C = X + (size_t)O * BJ_B;
+                    }
+                    g.ldc = dp;
+                    g.a16 = 1;
+                    g.b16 = 1;
+                    out.push_back(g);
+                }
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
 // host driver
 
 enum { V_Q0 = 0, V_QC, V_QN, V_QS, V_P, V_PH, V_PN, V_V0, V_GRAD, V_TV, V_BV, V_TMP, V_LAM0, V_LAM1, V_G0, V_G1 };
@@ -658,6 +898,45 @@ static double lg_hnorm(LgCtx &c) {
     return sqrt(c.sc[8]);
 }
 
+// Block Jacobi of H (symmetric) with V = P_dst on entry (identity when cold):
+// on exit H's diagonal holds the eigenvalues and P_dst the eigenvectors.
+static int lg_jacobi_block(LgCtx &c, int dst, double tol, double skip, int *sweeps) {
+    const int d = c.d, dp = c.L.bj_dp, nbk = c.L.bj_nbk, np = nbk / 2;
+    // P_dst holds the starting basis (identity when cold, the previous basis when warm)
+    k_bj_in<<<lg_blocks((size_t)dp * dp), 256, 0, c.s>>>(c.L.bjA, c.L.bjV[0], c.L.H, c.L.P[dst], d, dp, 0);
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(k_bj_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BJ_SMEM);
+        configured = true;
+    }
+    int vcur = 0, sw = 0;
+    const size_t per_round = (size_t)4 * np * 2;
+    const int nb_part = 148 * 2;
+    for (;;) {
+        k_bj_offnorm<<<nb_part, 256, 0, c.s>>>(c.L.bjA, dp, c.L.bjPart);
+        k_bj_offnorm_final<<<1, 32, 0, c.s>>>(c.L.bjPart, nb_part, c.L.sc + 7);
+        lg_sync(c);
+        if (c.sc[7] <= tol) break;
+        if (sw >= c.cfg.sweep_cap) {
+            *sweeps = -1;
+            return SGP_STATUS_JACOBI;
+        }
+        for (int r = 0; r < nbk - 1; ++r) {
+            const GemmArgs *D = c.L.bjDesc + (size_t)r * per_round;
+            k_bj_solve<<<np, 256, BJ_SMEM, c.s>>>(c.L.bjA, dp, r, nbk, skip, c.L.bjU, c.L.bjLam, c.L.bjCnt);
+            gemm_launch_batched<0, 0>(D, 2 * np, dp, BJ_B, c.s);                                  // T = A U (columns)
+            gemm_launch_batched<1, 0>(D + 2 * np, 2 * np, BJ_B, dp, c.s);                         // A = U^T T (rows)
+            gemm_launch_batched<0, 0>(D + (size_t)(vcur ? 3 : 2) * 2 * np, 2 * np, dp, BJ_B, c.s);  // V' = V U
+            k_bj_fix<<<np, 256, 0, c.s>>>(c.L.bjA, dp, r, nbk, c.L.bjLam, c.L.bjCnt);
+            vcur ^= 1;
+        }
+        ++sw;
+    }
+    k_bj_out<<<lg_blocks((size_t)d * d), 256, 0, c.s>>>(c.L.H, c.L.P[dst], c.L.bjA, c.L.bjV[vcur], d, dp);
+    *sweeps = sw;
+    return 0;
+}
+
 // Jacobi on H with V = P_dst: parallel (grid, round-robin) or reference order (one warp)
 static int lg_jacobi(LgCtx &c, int dst, double tol, double skip, bool parallel, int *sweeps) {
     const int d = c.d;
@@ -668,6 +947,8 @@ static int lg_jacobi(LgCtx &c, int dst, double tol, double skip, bool parallel, 
         *sweeps = c.si[4];
         return c.status;
     }
+    const char *sj = getenv("SGP_LG_SCALAR_JACOBI");
+    if (!(sj && sj[0] == '1') && c.L.bjA) return lg_jacobi_block(c, dst, tol, skip, sweeps);
     const int m = d + (d & 1), np = m >> 1;
     int sw = 0;
     for (;;) {
@@ -836,6 +1117,14 @@ static int lg_alloc(const ModelDev &M, LgPtrs &L, void **owner) {
                  osa = take(3 * (size_t)ld), ov = take(16 * (size_t)d), osc = take(16), osi = take(16),
                  ost = take(2), ojl = take(sgp_jacobi_log_doubles(d)), ojp = take(5 * np), ojq = take(2 * np),
                  ored = take(64);
+    // block Jacobi
+    const int nbk = ((d + 2 * BJ_B - 1) / (2 * BJ_B)) * 2, dp = nbk * BJ_B, bnp = nbk / 2;
+    const size_t dpp = (size_t)dp * dp;
+    const size_t obA = take(dpp), obT = take(dpp), obV0 = take(dpp), obV1 = take(dpp),
+                 obU = take((size_t)bnp * BJ_N * BJ_N), obL = take((size_t)bnp * BJ_N), obP = take(512),
+                 obC = take((size_t)bnp);
+    const size_t ndesc = (size_t)(nbk - 1) * 4 * bnp * 2;
+    const size_t obD = take((ndesc * sizeof(GemmArgs) + sizeof(double) - 1) / sizeof(double) + 2);
     double *base = nullptr;
     if (cudaMalloc(&base, off * sizeof(double)) != cudaSuccess) return SGP_ENOMEM;
     cudaMemset(base, 0, off * sizeof(double));
@@ -856,6 +1145,25 @@ static int lg_alloc(const ModelDev &M, LgPtrs &L, void **owner) {
     L.jprm = base + ojp;
     L.jpairs = reinterpret_cast<int *>(base + ojq);
     L.red = base + ored;
+    L.bj_dp = dp;
+    L.bj_nbk = nbk;
+    L.bjA = base + obA;
+    L.bjT = base + obT;
+    L.bjV[0] = base + obV0;
+    L.bjV[1] = base + obV1;
+    L.bjU = base + obU;
+    L.bjLam = base + obL;
+    L.bjPart = base + obP;
+    L.bjCnt = reinterpret_cast<int *>(base + obC);
+    L.bjDesc = reinterpret_cast<GemmArgs *>(base + ((obD + 1) & ~size_t(1)));  // 16-byte aligned
+    {
+        std::vector<GemmArgs> desc;
+        bj_build_desc(L, desc);
+        if (cudaMemcpy(L.bjDesc, desc.data(), desc.size() * sizeof(GemmArgs), cudaMemcpyHostToDevice) != cudaSuccess) {
+            cudaFree(base);
+            return SGP_ENOMEM;
+        }
+    }
     *owner = base;
     return SGP_OK;
 }
