@@ -41,6 +41,9 @@ struct GemmArgs {
     // non-null second base reads A2 / B2 at k - ksplit.  ksplit % GM_BK == 0.
     const double *A2, *B2;
     int ksplit;
+    // output split: rows m >= msplit (or columns n >= nsplit) go to C2 at m - msplit (n - nsplit)
+    double *C2;
+    int msplit, nsplit;
 };
 
 __device__ __forceinline__ void dmma_m8n8k4(double &c0, double &c1, double a, double b) {
@@ -213,7 +216,13 @@ __device__ __forceinline__ void gm_body(const GemmArgs &g) {
                 const int n = n0 + wn + j * 8 + 2 * tig + h;
                 if (n >= g.N) continue;
                 double v = g.alpha * acc[i][j][h];
-                double *cp = g.C + (size_t)m * g.ldc + n;
+                double *cp;
+                if (g.C2 && g.nsplit && n >= g.nsplit)
+                    cp = g.C2 + (size_t)m * g.ldc + (n - g.nsplit);
+                else if (g.C2 && g.msplit && m >= g.msplit)
+                    cp = g.C2 + (size_t)(m - g.msplit) * g.ldc + n;
+                else
+                    cp = g.C + (size_t)m * g.ldc + n;
                 if (g.beta != 0.0) v += g.beta * *cp;
                 *cp = v;
             }

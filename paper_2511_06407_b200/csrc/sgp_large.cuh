@@ -551,7 +551,7 @@ __host__ __device__ inline void bj_pair(int r, int k, int nbk, int &I, int &J) {
 }
 
 __global__ void __launch_bounds__(256) k_bj_solve(const double *A, int dp, int r, int nbk, double skip, double *Uall,
-                                                  double *lamall, int *cnt) {
+                                                  double *lamall, int *cnt, int inner_cap) {
     extern __shared__ double bjsm[];  // S and U, rows padded to BJ_N + 1
     double(*S)[BJ_N + 1] = reinterpret_cast<double(*)[BJ_N + 1]>(bjsm);
     double(*U)[BJ_N + 1] = reinterpret_cast<double(*)[BJ_N + 1]>(bjsm + BJ_N * (BJ_N + 1));
@@ -571,7 +571,7 @@ __global__ void __launch_bounds__(256) k_bj_solve(const double *A, int dp, int r
     if (tid == 0) nrot = 0;
     __syncthreads();
     constexpr int m = BJ_N, np = BJ_N / 2;
-    for (int sweep = 0; sweep < BJ_INNER_CAP; ++sweep) {
+    for (int sweep = 0; sweep < inner_cap; ++sweep) {
         if (tid == 0) any = 0;
         __syncthreads();
         for (int rr = 0; rr < m - 1; ++rr) {
@@ -642,11 +642,13 @@ __global__ void __launch_bounds__(256) k_bj_solve(const double *A, int dp, int r
     }
     double *Uk = Uall + (size_t)k * BJ_N * BJ_N;
     for (int idx = tid; idx < BJ_N * BJ_N; idx += blockDim.x) Uk[idx] = U[idx / BJ_N][idx % BJ_N];
-    for (int i = tid; i < BJ_N; i += blockDim.x) lamall[(size_t)k * BJ_N + i] = S[i][i];
+    // the transformed subproblem (diagonal when the inner sweeps converged)
+    for (int idx = tid; idx < BJ_N * BJ_N; idx += blockDim.x) lamall[(size_t)k * BJ_N * BJ_N + idx] = S[idx / BJ_N][idx % BJ_N];
     if (tid == 0) cnt[k] = nrot;
 }
 
-// exact diagonal blocks of every pair after its transformation: diag(lambda), zeros
+// diagonal blocks of every pair after its transformation: the inner solver's
+// transformed subproblem (exact zeros where it annihilated, as the reference does)
 __global__ void k_bj_fix(double *A, int dp, int r, int nbk, const double *lamall, const int *cnt) {
     const int k = blockIdx.x;
     if (!cnt[k]) return;
@@ -656,7 +658,7 @@ __global__ void k_bj_fix(double *A, int dp, int r, int nbk, const double *lamall
         const int i = idx / BJ_N, j = idx - i * BJ_N;
         const int gi = i < BJ_B ? I * BJ_B + i : J * BJ_B + i - BJ_B;
         const int gj = j < BJ_B ? I * BJ_B + j : J * BJ_B + j - BJ_B;
-        A[(size_t)gi * dp + gj] = i == j ? lamall[(size_t)k * BJ_N + i] : 0.0;
+        A[(size_t)gi * dp + gj] = lamall[(size_t)k * BJ_N * BJ_N + idx];
     }
 }
 
@@ -705,7 +707,9 @@ __global__ void k_bj_out(double *H, double *P, const double *Ap, const double *V
     }
 }
 
-// Descriptors of the three batched update GEMMs of every round (host side).
+// Descriptors of the three batched update GEMMs of every round (host side):
+// one 64-wide GEMM per pair and kind, K gathered from blocks I and J and the
+// output split back into blocks I and J.
 static void bj_build_desc(const LgPtrs &L, std::vector<GemmArgs> &out) {
     const int dp = L.bj_dp, nbk = L.bj_nbk, np = nbk / 2;
     out.clear();
@@ -715,42 +719,43 @@ static void bj_build_desc(const LgPtrs &L, std::vector<GemmArgs> &out) {
                 int I, J;
                 bj_pair(r, k, nbk, I, J);
                 const double *Uk = L.bjU + (size_t)k * BJ_N * BJ_N;
-                for (int h = 0; h < 2; ++h) {
-                    const int O = h ? J : I;
-                    GemmArgs g{};
-                    g.alpha = 1.0;
-                    g.beta = 0.0;
-                    g.K = BJ_N;
-                    g.ksplit = BJ_B;
-                    if (kind == 1) {
-                        // A[O rows, :] = U[:, h]^T T[I|J rows, :]
-                        g.M = BJ_B;
-                        g.N = dp;
-                        g.A = Uk + h * BJ_B;
-                        g.lda = BJ_N;
-                        g.TA = 1;
-                        g.B = L.bjT + (size_t)I * BJ_B * dp;
-                        g.B2 = L.bjT + (size_t)J * BJ_B * dp;
-                        g.ldb = dp;
-                        g.C = L.bjA + (size_t)O * BJ_B * dp;
-                    } else {
-                        // X[:, O cols] = Y[:, I|J cols] U[:, h]
-                        const double *Y = kind == 0 ? L.bjA : (kind == 2 ? L.bjV[0] : L.bjV[1]);
-                        double *X = kind == 0 ? L.bjT : (kind == 2 ? L.bjV[1] : L.bjV[0]);
-                        g.M = dp;
-                        g.N = BJ_B;
-                        g.A = Y + (size_t)I * BJ_B;
-                        g.A2 = Y + (size_t)J * BJ_B;
-                        g.lda = dp;
-                        g.B = Uk + h * BJ_B;
-                        g.ldb = BJ_N;
-                        g.C = X + (size_t)O * BJ_B;
-                    }
-                    g.ldc = dp;
-                    g.a16 = 1;
-                    g.b16 = 1;
-                    out.push_back(g);
+                GemmArgs g{};
+                g.alpha = 1.0;
+                g.beta = 0.0;
+                g.K = BJ_N;
+                g.ksplit = BJ_B;
+                if (kind == 1) {
+                    // A[I|J rows, :] = U^T T[I|J rows, :]
+                    g.M = BJ_N;
+                    g.N = dp;
+                    g.A = Uk;
+                    g.lda = BJ_N;
+                    g.TA = 1;
+                    g.B = L.bjT + (size_t)I * BJ_B * dp;
+                    g.B2 = L.bjT + (size_t)J * BJ_B * dp;
+                    g.ldb = dp;
+                    g.C = L.bjA + (size_t)I * BJ_B * dp;
+                    g.C2 = L.bjA + (size_t)J * BJ_B * dp;
+                    g.msplit = BJ_B;
+                } else {
+                    // X[:, I|J cols] = Y[:, I|J cols] U
+                    const double *Y = kind == 0 ? L.bjA : (kind == 2 ? L.bjV[0] : L.bjV[1]);
+                    double *X = kind == 0 ? L.bjT : (kind == 2 ? L.bjV[1] : L.bjV[0]);
+                    g.M = dp;
+                    g.N = BJ_N;
+                    g.A = Y + (size_t)I * BJ_B;
+                    g.A2 = Y + (size_t)J * BJ_B;
+                    g.lda = dp;
+                    g.B = Uk;
+                    g.ldb = BJ_N;
+                    g.C = X + (size_t)I * BJ_B;
+                    g.C2 = X + (size_t)J * BJ_B;
+                    g.nsplit = BJ_B;
                 }
+                g.ldc = dp;
+                g.a16 = 1;
+                g.b16 = 1;
+                out.push_back(g);
             }
         }
     }
@@ -905,12 +910,15 @@ static int lg_jacobi_block(LgCtx &c, int dst, double tol, double skip, int *swee
     // P_dst holds the starting basis (identity when cold, the previous basis when warm)
     k_bj_in<<<lg_blocks((size_t)dp * dp), 256, 0, c.s>>>(c.L.bjA, c.L.bjV[0], c.L.H, c.L.P[dst], d, dp, 0);
     static bool configured = false;
+    static int inner_cap = 1;
     if (!configured) {
         cudaFuncSetAttribute(k_bj_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BJ_SMEM);
+        const char *e = getenv("SGP_BJ_INNER");  // inner sweeps per pair subproblem (tuning)
+        if (e && atoi(e) > 0) inner_cap = atoi(e);
         configured = true;
     }
     int vcur = 0, sw = 0;
-    const size_t per_round = (size_t)4 * np * 2;
+    const size_t per_round = (size_t)4 * np;
     const int nb_part = 148 * 2;
     for (;;) {
         k_bj_offnorm<<<nb_part, 256, 0, c.s>>>(c.L.bjA, dp, c.L.bjPart);
@@ -923,10 +931,11 @@ static int lg_jacobi_block(LgCtx &c, int dst, double tol, double skip, int *swee
         }
         for (int r = 0; r < nbk - 1; ++r) {
             const GemmArgs *D = c.L.bjDesc + (size_t)r * per_round;
-            k_bj_solve<<<np, 256, BJ_SMEM, c.s>>>(c.L.bjA, dp, r, nbk, skip, c.L.bjU, c.L.bjLam, c.L.bjCnt);
-            gemm_launch_batched<0, 0>(D, 2 * np, dp, BJ_B, c.s);                                  // T = A U (columns)
-            gemm_launch_batched<1, 0>(D + 2 * np, 2 * np, BJ_B, dp, c.s);                         // A = U^T T (rows)
-            gemm_launch_batched<0, 0>(D + (size_t)(vcur ? 3 : 2) * 2 * np, 2 * np, dp, BJ_B, c.s);  // V' = V U
+            k_bj_solve<<<np, 256, BJ_SMEM, c.s>>>(c.L.bjA, dp, r, nbk, skip, c.L.bjU, c.L.bjLam, c.L.bjCnt,
+                                                  inner_cap);
+            gemm_launch_batched<0, 0>(D, np, dp, BJ_N, c.s);                            // T = A U (columns)
+            gemm_launch_batched<1, 0>(D + np, np, BJ_N, dp, c.s);                       // A = U^T T (rows)
+            gemm_launch_batched<0, 0>(D + (size_t)(vcur ? 3 : 2) * np, np, dp, BJ_N, c.s);  // V' = V U
             k_bj_fix<<<np, 256, 0, c.s>>>(c.L.bjA, dp, r, nbk, c.L.bjLam, c.L.bjCnt);
             vcur ^= 1;
         }
@@ -1121,9 +1130,9 @@ static int lg_alloc(const ModelDev &M, LgPtrs &L, void **owner) {
     const int nbk = ((d + 2 * BJ_B - 1) / (2 * BJ_B)) * 2, dp = nbk * BJ_B, bnp = nbk / 2;
     const size_t dpp = (size_t)dp * dp;
     const size_t obA = take(dpp), obT = take(dpp), obV0 = take(dpp), obV1 = take(dpp),
-                 obU = take((size_t)bnp * BJ_N * BJ_N), obL = take((size_t)bnp * BJ_N), obP = take(512),
+                 obU = take((size_t)bnp * BJ_N * BJ_N), obL = take((size_t)bnp * BJ_N * BJ_N), obP = take(512),
                  obC = take((size_t)bnp);
-    const size_t ndesc = (size_t)(nbk - 1) * 4 * bnp * 2;
+    const size_t ndesc = (size_t)(nbk - 1) * 4 * bnp;
     const size_t obD = take((ndesc * sizeof(GemmArgs) + sizeof(double) - 1) / sizeof(double) + 2);
     double *base = nullptr;
     if (cudaMalloc(&base, off * sizeof(double)) != cudaSuccess) return SGP_ENOMEM;
