@@ -514,7 +514,8 @@ __device__ __noinline__ void eval_state(EvalCtx &E, const double *q, double tau,
     bool bad = false;
     if (what & SGP_EVAL_GRADIENT)
         for (int a = threadIdx.x; a < d; a += SGP_NT) bad |= !isfinite(grad[a]);
-    if (what & SGP_EVAL_HESSIAN)
+    // (large-d path: the d x d scan runs on the grid, k_lg_finite)
+    if ((what & SGP_EVAL_HESSIAN) && !(what & SGP_EVAL_HPRIOR))
         for (int idx = threadIdx.x; idx < d * d; idx += SGP_NT) bad |= !isfinite(H[idx]);
     if ((what & SGP_EVAL_POTENTIAL) && threadIdx.x == 0 && !isfinite(o.pot)) bad = true;
     if (bad) set_status(E.status, SGP_STATUS_DIVERGENCE);

@@ -550,7 +550,8 @@ __host__ __device__ inline void bj_pair(int r, int k, int nbk, int &I, int &J) {
     J = a < b ? b : a;
 }
 
-__global__ void __launch_bounds__(256) k_bj_solve(const double *A, int dp, int r, int nbk, double skip, double *Uall,
+#define BJ_SOLVE_NT 1024
+__global__ void __launch_bounds__(BJ_SOLVE_NT) k_bj_solve(const double *A, int dp, int r, int nbk, double skip, double *Uall,
                                                   double *lamall, int *cnt, int inner_cap) {
     extern __shared__ double bjsm[];  // S and U, rows padded to BJ_N + 1
     double(*S)[BJ_N + 1] = reinterpret_cast<double(*)[BJ_N + 1]>(bjsm);
@@ -589,7 +590,7 @@ __global__ void __launch_bounds__(256) k_bj_solve(const double *A, int dp, int r
                 const bool act = fabs(apq) > skip;
                 double c = 1.0, sn = 0.0, t = 0.0;
                 const double app = S[p][p], aqq = S[q][q];
-                if (act) jacobi_rot(app, aqq, apq, c, sn, t);
+                if (act && !jacobi_rot_fast(app, aqq, apq, c, sn, t)) jacobi_rot(app, aqq, apq, c, sn, t);
                 rc[tid] = c;
                 rs[tid] = sn;
                 rt[tid] = t * apq;
@@ -678,6 +679,35 @@ __global__ void k_bj_offnorm(const double *A, int dp, double *part) {
         double t = 0.0;
         for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
         part[blockIdx.x] = t;
+    }
+}
+// non-finite Hessian entry -> DivergenceError (posterior.py:479)
+__global__ void k_lg_finite(const double *H, size_t n, int *status) {
+    bool bad = false;
+    for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < n; idx += (size_t)gridDim.x * blockDim.x)
+        bad |= !isfinite(H[idx]);
+    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicCAS(status, 0, SGP_STATUS_DIVERGENCE);
+}
+
+__global__ void k_bj_sumsq(const double *A, size_t n, double *part) {
+    __shared__ double red[32];
+    double s = 0.0;
+    for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < n; idx += (size_t)gridDim.x * blockDim.x)
+        s += A[idx] * A[idx];
+    s = warp_sum(s);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+        part[blockIdx.x] = t;
+    }
+}
+__global__ void k_bj_sum_final(const double *part, int n, double *out) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        double t = 0.0;
+        for (int i = 0; i < n; ++i) t += part[i];
+        *out = t;
     }
 }
 __global__ void k_bj_offnorm_final(const double *part, int n, double *out) {
@@ -863,6 +893,7 @@ static int lg_state(LgCtx &c, int qv, int what) {
                 }
         }
         lg_op(c, LG_STATE, 0, qv, 0, SGP_EVAL_HESSIAN | SGP_EVAL_HPRIOR | SGP_EVAL_REUSE);
+        k_lg_finite<<<lg_blocks((size_t)d * d), 256, 0, c.s>>>(c.L.H, (size_t)d * d, c.L.status);
     }
     return lg_sync(c);
 }
@@ -898,7 +929,10 @@ static int lg_trace(LgCtx &c, int qv) {
 }
 
 static double lg_hnorm(LgCtx &c) {
-    k_lg_frob<<<1, 1024, 0, c.s>>>(c.L.H, (size_t)c.d * c.d, c.L.sc + 8);
+    // ||H||_F^2 as per-block partials and one ordered sum (deterministic)
+    const int nb = 148 * 2;
+    k_bj_sumsq<<<nb, 256, 0, c.s>>>(c.L.H, (size_t)c.d * c.d, c.L.bjPart);
+    k_bj_sum_final<<<1, 32, 0, c.s>>>(c.L.bjPart, nb, c.L.sc + 8);
     lg_sync(c);
     return sqrt(c.sc[8]);
 }
@@ -931,7 +965,7 @@ static int lg_jacobi_block(LgCtx &c, int dst, double tol, double skip, int *swee
         }
         for (int r = 0; r < nbk - 1; ++r) {
             const GemmArgs *D = c.L.bjDesc + (size_t)r * per_round;
-            k_bj_solve<<<np, 256, BJ_SMEM, c.s>>>(c.L.bjA, dp, r, nbk, skip, c.L.bjU, c.L.bjLam, c.L.bjCnt,
+            k_bj_solve<<<np, BJ_SOLVE_NT, BJ_SMEM, c.s>>>(c.L.bjA, dp, r, nbk, skip, c.L.bjU, c.L.bjLam, c.L.bjCnt,
                                                   inner_cap);
             gemm_launch_batched<0, 0>(D, np, dp, BJ_N, c.s);                            // T = A U (columns)
             gemm_launch_batched<1, 0>(D + np, np, BJ_N, dp, c.s);                       // A = U^T T (rows)
