@@ -681,6 +681,47 @@ __global__ void k_bj_offnorm(const double *A, int dp, double *part) {
         part[blockIdx.x] = t;
     }
 }
+// ---- grid mat-vecs of the metric algebra (metric.py:188-241) at large d ----
+#define LG_TV_KS 16
+// part[ks][j] = sum_{k in chunk ks} P[k][j] v[k]   (Psi^T v, coalesced over j)
+__global__ void k_lg_tvec_part(const double *P, const double *v, int d, double *part) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x, ks = blockIdx.y;
+    const int chunk = (d + LG_TV_KS - 1) / LG_TV_KS, k0 = ks * chunk, k1 = min(d, k0 + chunk);
+    if (j >= d) return;
+    double s = 0.0;
+    for (int k = k0; k < k1; ++k) s += P[(size_t)k * d + j] * v[k];
+    part[(size_t)ks * d + j] = s;
+}
+// out[j] = f(sum_ks part[ks][j]): mode 0: /g, 1: *g, 3: plain; 4: kinetic terms t^2/g into out
+__global__ void k_lg_tvec_fin(const double *part, const double *g, int d, int mode, double *out) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= d) return;
+    double s = 0.0;
+    for (int ks = 0; ks < LG_TV_KS; ++ks) s += part[(size_t)ks * d + j];
+    out[j] = mode == 0 ? s / g[j] : (mode == 1 ? g[j] * s : (mode == 4 ? s * s / g[j] : s));
+}
+// out[j] = sum_k P[j][k] t[k]   (Psi t, one warp per row)
+__global__ void k_lg_vec(const double *P, const double *t, int d, double *out) {
+    const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, l = threadIdx.x & 31;
+    if (w >= d) return;
+    double s = 0.0;
+    for (int k = l; k < d; k += 32) s += P[(size_t)w * d + k] * t[k];
+    s = warp_sum(s);
+    if (l == 0) out[w] = s;
+}
+__global__ void k_lg_sqrtg_v(const double *g, const double *v, int d, double *out) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j < d) out[j] = sqrt(g[j]) * v[j];
+}
+// sc[6] = 0.5 * sum(terms) + 0.5 (d ln 2 pi + logdet)   (one warp, ordered)
+__global__ void k_lg_kinetic_fin(const double *terms, int d, const double *sc_logdet, double *out) {
+    const int l = threadIdx.x;
+    double s = 0.0;
+    for (int k = l; k < d; k += 32) s += terms[k];
+    s = warp_sum(s);
+    if (l == 0) *out = 0.5 * s + 0.5 * (d * SGP_LN_2PI + *sc_logdet);
+}
+
 // non-finite Hessian entry -> DivergenceError (posterior.py:479)
 __global__ void k_lg_finite(const double *H, size_t n, int *status) {
     bool bad = false;
@@ -833,6 +874,23 @@ static int lg_sync(LgCtx &c) {
 
 static void lg_clear_status(LgCtx &c) { cudaMemsetAsync(c.L.status, 0, sizeof(int), c.s); }
 
+// grid versions of LG_BVEC / LG_APPLY / LG_KINETIC (same formulas as metric_apply etc.)
+static void lg_tvec(LgCtx &c, int slot, const double *v, int mode, double *out) {
+    const int d = c.d;
+    k_lg_tvec_part<<<dim3((d + 127) / 128, LG_TV_KS), 128, 0, c.s>>>(c.L.P[slot], v, d, c.L.X);
+    k_lg_tvec_fin<<<(d + 127) / 128, 128, 0, c.s>>>(c.L.X, c.L.vec + (size_t)(14 + slot) * d, d, mode, out);
+}
+static void lg_apply_g(LgCtx &c, int slot, int vin, int vout, int mode) {
+    const int d = c.d;
+    double *tmp = c.L.vec + (size_t)10 * d;  // V_BV, clobbered as in metric_apply
+    const double *g = c.L.vec + (size_t)(14 + slot) * d;
+    if (mode == 2)
+        k_lg_sqrtg_v<<<(d + 127) / 128, 128, 0, c.s>>>(g, c.L.vec + (size_t)vin * d, d, tmp);
+    else
+        lg_tvec(c, slot, c.L.vec + (size_t)vin * d, mode, tmp);
+    k_lg_vec<<<(d * 32 + 255) / 256, 256, 0, c.s>>>(c.L.P[slot], tmp, d, c.L.vec + (size_t)vout * d);
+}
+
 static void lg_gemm(LgCtx &c, int M, int N, int K, const double *A, int lda, int TA, const double *B, int ldb, int TB,
                     const double *scale, double *C, int ldc, double alpha, int upper) {
     GemmArgs g{};
@@ -901,7 +959,7 @@ static int lg_state(LgCtx &c, int qv, int what) {
 // W = Psi_slot (diag r - (b b^T) o T) Psi_slot^T, b from vec[pv]
 static void lg_contraction(LgCtx &c, int slot, int pv) {
     const int d = c.d;
-    lg_op(c, LG_BVEC, slot, pv);
+    lg_tvec(c, slot, c.L.vec + (size_t)pv * d, 0, c.L.vec + (size_t)V_BV * d);
     k_lg_mmat<<<lg_blocks((size_t)d * d), 256, 0, c.s>>>(c.L, slot, c.cfg.kappa, -1.0, 1, 1);
     lg_gemm(c, d, d, d, c.L.P[slot], d, 0, c.L.W, d, 0, nullptr, c.L.X, d, 1.0, 0);  // X = Psi M
     lg_gemm(c, d, d, d, c.L.X, d, 0, c.L.P[slot], d, 1, nullptr, c.L.W, d, 1.0, 1);  // W = X Psi^T
@@ -1088,7 +1146,7 @@ static int lg_leapfrog(LgCtx &c, int &f, int *fp_p, int *fp_q, double *sweep_sum
         }
     }
     if (!conv) return SGP_STATUS_STALL_P;
-    lg_op(c, LG_APPLY, f, V_PH, V_V0, 0);
+    lg_apply_g(c, f, V_PH, V_V0, 0);
     // qc = q0 + eps v0 (QDELTA with the roles shifted: use tmp = v0 -> qn = q0 + eps v0)
     cudaMemcpyAsync(c.L.vec + (size_t)V_TMP * d, c.L.vec + (size_t)V_V0 * d, sizeof(double) * d,
                     cudaMemcpyDeviceToDevice, c.s);
@@ -1107,7 +1165,7 @@ static int lg_leapfrog(LgCtx &c, int &f, int *fp_p, int *fp_q, double *sweep_sum
         *sweep_sum += sw;
         ++*sweep_cnt;
         cur = nxt;
-        lg_op(c, LG_APPLY, cur, V_PH, V_TMP, 0);
+        lg_apply_g(c, cur, V_PH, V_TMP, 0);
         lg_op(c, LG_QDELTA, 0, 0, 0, 0, eps);
         lg_sync(c);
         if (c.sc[5] <= c.cfg.fp_tol) {
@@ -1282,7 +1340,8 @@ static double lg_kinetic(LgCtx &c, int f) {
         for (double v : p) s += v * v;
         return 0.5 * s + 0.5 * c.d * SGP_LN_2PI;
     }
-    lg_op(c, LG_KINETIC, f);
+    lg_tvec(c, f, c.L.vec + (size_t)V_P * c.d, 4, c.L.vec + (size_t)V_BV * c.d);
+    k_lg_kinetic_fin<<<1, 32, 0, c.s>>>(c.L.vec + (size_t)V_BV * c.d, c.d, c.L.sc + f, c.L.sc + 6);
     lg_sync(c);
     return c.sc[6];
 }
@@ -1351,7 +1410,7 @@ static int lg_run_moves(const LgPtrs &L, const sgp_chain_config *cfg, const sgp_
                 cudaMemcpyAsync(L.vec + (size_t)V_P * d, zz, sizeof(double) * d, cudaMemcpyDeviceToDevice, s);
             } else {
                 cudaMemcpyAsync(L.vec + (size_t)V_PN * d, zz, sizeof(double) * d, cudaMemcpyDeviceToDevice, s);
-                lg_op(c, LG_APPLY, f, V_PN, V_P, 2);
+                lg_apply_g(c, f, V_PN, V_P, 2);
             }
             lg_sync(c);
             const double pot_before = c.sc[2];
