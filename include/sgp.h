@@ -227,6 +227,29 @@ int sgp_run_moves(const sgp_model *model, const sgp_chain_config *cfg,
                   const double *d_z, const double *d_logu, sgp_move_records *rec,
                   void *stream);
 
+/* Laplace-grid evidence oracle (replaces evidence.py:330-426
+ * laplace_grid_oracle's node loop).  The grid of
+ * (c_g, sigma_g) midpoints is round(c_max/c_mesh) x round(sigma_max/sigma_mesh)
+ * nodes in the reference's serpentine order; every node optimises the
+ * coefficient block in prior-whitened coordinates with the reference's
+ * L-BFGS (memory, strong Wolfe search, gtol, max_iters) from a = 0 and
+ * Cholesky-factorises the coefficient Hessian block.  Outputs per node, on the
+ * host: the node log-evidence term (evidence.py:403-410), a status (0 ok,
+ * 1 optimiser did not converge, 2 Cholesky failed, 3 objective not finite at
+ * the start) and the L-BFGS iteration count.  The caller validates the model
+ * (both Gaussian-kernel hypers sampled, others pinned) and combines the nodes
+ * (skip tolerance, log-sum-exp).  Models on the large-d path are rejected. */
+typedef struct {
+    double c_max, c_mesh, sigma_max, sigma_mesh;
+    int n_pinned;
+    int pinned_pos[3];       /* sampled coordinates of pinned hypers */
+    double pinned_value[3];  /* their sampled-coordinate values (ln value for the log transform) */
+    double gtol;
+    int max_iters, memory;
+} sgp_grid_spec;
+int sgp_laplace_grid(const sgp_model *model, const sgp_grid_spec *spec, int n_nodes, double *h_values,
+                     int *h_status, int *h_iters, void *stream);
+
 /* Diagnostics: cycles spent by chain 0 in each leapfrog phase (clock64), 16
  * slots: 0 W formation, 1 trace contraction, 2 state + Hessian, 3 MGS,
  * 4 Psi^T H Psi, 5 warm Jacobi, 8 cold Jacobi, 9 whole leapfrog. */

@@ -840,3 +840,238 @@ def thermo_integrate(target, taus, moves_per_rung, leapfrogs, chains, cfg, *,
         except OChainError:
             per_chain.append(math.nan)
     return per_chain, rung_values, q_warm
+
+
+# ---------------------------------------------------------------------------
+# Laplace evidence oracles: L-BFGS, laplace_full,
+# laplace_grid_oracle.
+
+@dataclasses.dataclass
+class OOptim:
+    x: np.ndarray
+    value: float
+    grad: np.ndarray
+    iterations: int
+    evaluations: int
+    converged: bool
+
+
+def _two_loop(grad, s_hist, y_hist, rho_hist):
+    """lbfgs.py:27-40."""
+    q = grad.copy()
+    alphas = []
+    for s, y, rho in zip(reversed(s_hist), reversed(y_hist), reversed(rho_hist)):
+        a = rho * float(s @ q)
+        alphas.append(a)
+        q -= a * y
+    if y_hist:
+        q *= float(s_hist[-1] @ y_hist[-1]) / float(y_hist[-1] @ y_hist[-1])
+    for (s, y, rho), a in zip(zip(s_hist, y_hist, rho_hist), reversed(alphas)):
+        b = rho * float(y @ q)
+        q += (a - b) * s
+    return q
+
+
+def _zoom(fg, x, d, f0, dphi0, lo, f_lo, hi, c1, c2, max_iter=30):
+    """lbfgs.py:43-64: bisection zoom of the strong Wolfe search."""
+    evals = 0
+    for _ in range(max_iter):
+        a = 0.5 * (lo + hi)
+        f, g = fg(x + a * d)
+        evals += 1
+        dphi = float(g @ d) if math.isfinite(f) else math.inf
+        if not math.isfinite(f) or f > f0 + c1 * a * dphi0 or f >= f_lo:
+            hi = a
+        else:
+            if abs(dphi) <= -c2 * dphi0:
+                return a, f, g, evals
+            if dphi * (hi - lo) >= 0.0:
+                hi = lo
+            lo, f_lo = a, f
+        if abs(hi - lo) <= 1e-14 * max(1.0, abs(lo)):
+            break
+    f, g = fg(x + lo * d)
+    evals += 1
+    if math.isfinite(f) and f <= f0 + c1 * lo * dphi0 and lo > 0.0:
+        return lo, f, g, evals
+    return None, f0, None, evals
+
+
+def _wolfe(fg, x, f0, g0, d, c1, c2, max_expand=25):
+    """lbfgs.py:67-86: expanding strong Wolfe line search."""
+    dphi0 = float(g0 @ d)
+    a_prev, f_prev, a, evals = 0.0, f0, 1.0, 0
+    for i in range(max_expand):
+        f, g = fg(x + a * d)
+        evals += 1
+        if not math.isfinite(f) or f > f0 + c1 * a * dphi0 or (i > 0 and f >= f_prev):
+            r = _zoom(fg, x, d, f0, dphi0, a_prev, f_prev, a, c1, c2)
+            return r[0], r[1], r[2], evals + r[3]
+        dphi = float(g @ d)
+        if abs(dphi) <= -c2 * dphi0:
+            return a, f, g, evals
+        if dphi >= 0.0:
+            r = _zoom(fg, x, d, f0, dphi0, a, f, a_prev, c1, c2)
+            return r[0], r[1], r[2], evals + r[3]
+        a_prev, f_prev = a, f
+        a *= 2.0
+    return None, f0, None, evals
+
+
+def lbfgs_minimize(fg, x0, *, memory=10, gtol=1e-6, max_iters=200, c1=1e-4, c2=0.9):
+    """lbfgs.py:89-150."""
+    x = np.asarray(x0, dtype=float).copy()
+    f, g = fg(x)
+    evals = 1
+    if not math.isfinite(f):
+        raise ValueError("objective is not finite at the starting point")
+    sh, yh, rh = [], [], []
+    for it in range(max_iters):
+        if float(np.max(np.abs(g))) <= gtol:
+            return OOptim(x, f, g, it, evals, True)
+        d = -_two_loop(g, sh, yh, rh)
+        if float(g @ d) >= 0.0:
+            sh.clear(), yh.clear(), rh.clear()
+            d = -g
+        alpha, fn, gn, ne = _wolfe(fg, x, f, g, d, c1, c2)
+        evals += ne
+        if alpha is None and sh:
+            sh.clear(), yh.clear(), rh.clear()
+            d = -g
+            alpha, fn, gn, ne = _wolfe(fg, x, f, g, d, c1, c2)
+            evals += ne
+        if alpha is None:
+            return OOptim(x, f, g, it, evals, float(np.max(np.abs(g))) <= gtol)
+        xn = x + alpha * d
+        s, y = xn - x, gn - g
+        sy = float(s @ y)
+        if sy > 1e-12 * float(np.linalg.norm(s)) * float(np.linalg.norm(y)):
+            sh.append(s), yh.append(y), rh.append(1.0 / sy)
+            if len(sh) > memory:
+                sh.pop(0), yh.pop(0), rh.pop(0)
+        x, f, g = xn, fn, gn
+    return OOptim(x, f, g, max_iters, evals, float(np.max(np.abs(g))) <= gtol)
+
+
+def prior_scales(target, q):
+    """posterior.py:289-307: 1/sqrt(r) per coefficient, sqrt(Sigma) per intercept."""
+    scales = np.ones(target.dim)
+    for g in target.groups:
+        hvals = tuple(q[p] for p in g.hpos)
+        scales[g.idx] = np.exp(-0.5 * _group_derivs(g, hvals, target.model.hyper_transform)["rho"])
+    for pos in target.inter:
+        scales[pos] = math.sqrt(target.model.intercept_variance)
+    return scales
+
+
+def hyperprior_potential(target, q):
+    """posterior.py:281-287."""
+    return float(sum(_hyperprior(target.hprior[n], target.model.hyper_transform, q[p])[0]
+                     for n, p in target.hidx.items()))
+
+
+LAPLACE_ZETA = 1e-13  # evidence.py:31
+
+
+def laplace_full(target, *, initial=None, gtol=1e-6, max_iters=500):
+    """evidence.py:277-304: -U(q*) + d/2 ln 2 pi - 1/2 ln|H(q*)| (Jacobi eigenvalues)."""
+    x0 = target.initial_point() if initial is None else np.asarray(initial, dtype=float)
+
+    def fg(x):
+        try:
+            p = target.at(x)
+            return p.potential(), p.gradient()
+        except (ODomain, ODivergence):
+            return math.inf, np.zeros(target.dim)
+
+    res = lbfgs_minimize(fg, x0, gtol=gtol, max_iters=max_iters)
+    if not res.converged:
+        raise RuntimeError("Laplace mode search did not reach gradient tolerance")
+    lam, _, _ = cold_eigh(target.at(res.x).hessian(), LAPLACE_ZETA)
+    if np.min(lam) <= 0.0:
+        raise RuntimeError("Laplace invalid (singular/indefinite posterior)")
+    return -res.value + 0.5 * target.dim * LN_2PI - 0.5 * float(np.sum(np.log(lam)))
+
+
+def _inv_gamma_logpdf(theta, alpha, beta):
+    """evidence.py:326-327."""
+    return alpha * math.log(beta) - math.lgamma(alpha) - (alpha + 1.0) * math.log(theta) - beta / theta
+
+
+def grid_centers(c_max, c_mesh, sigma_max, sigma_mesh):
+    """evidence.py:318-323 (GridSpec.centers)."""
+    nc, ns = int(round(c_max / c_mesh)), int(round(sigma_max / sigma_mesh))
+    return (np.arange(nc) + 0.5) * c_mesh, (np.arange(ns) + 0.5) * sigma_mesh
+
+
+def laplace_grid_nodes(target, c_max=4.0, c_mesh=0.01, sigma_max=4.0, sigma_mesh=0.02, pinned=(),
+                       *, gtol=1e-6, max_iters=200, warm="serpentine"):
+    """evidence.py:330-410: per-node conditional Laplace values in the reference's
+    serpentine order.  warm="serpentine" warm-starts each node from the previous
+    optimum (the reference); warm="zero" starts every node at a = 0 (the
+    device's independent nodes).  Returns (values in node order or nan, status
+    0 ok / 1 optimiser failed / 2 Cholesky failed, (c, sigma) per node)."""
+    model = target.model
+    pinned = dict(pinned)
+    hidx = target.hidx
+    transform = model.hyper_transform
+    coef_idx = np.array([i for i in range(target.dim) if i not in hidx.values()], dtype=int)
+    base = np.zeros(target.dim)
+    for name, value in pinned.items():
+        base[hidx[name]] = math.log(value) if transform == "log" else value
+    c_pos, s_pos = hidx["c_g"], hidx["sigma_g"]
+    prior_c, prior_s = model.priors["c_g"], model.priors["sigma_g"]
+    c_centers, s_centers = grid_centers(c_max, c_mesh, sigma_max, sigma_mesh)
+    log_area = math.log(c_mesh) + math.log(sigma_mesh)
+    n_coef = coef_idx.size
+    vals, stat, nodes = [], [], []
+    a_warm = np.zeros(n_coef)
+    for si, sigma in enumerate(s_centers):
+        row = c_centers if si % 2 == 0 else c_centers[::-1]
+        for c in row:
+            nodes.append((c, sigma))
+            q = base.copy()
+            q[c_pos] = math.log(c) if transform == "log" else c
+            q[s_pos] = math.log(sigma) if transform == "log" else sigma
+            scales = prior_scales(target, q)[coef_idx]
+
+            def fg(avec, q=q, scales=scales):
+                qq = q.copy()
+                qq[coef_idx] = avec * scales
+                try:
+                    p = target.at(qq)
+                    return p.potential(), p.gradient()[coef_idx] * scales
+                except (ODomain, ODivergence):
+                    return math.inf, np.zeros(n_coef)
+
+            start = a_warm / scales if warm == "serpentine" else np.zeros(n_coef)
+            res = lbfgs_minimize(fg, start, gtol=gtol, max_iters=max_iters)
+            if not res.converged:
+                vals.append(float("nan")), stat.append(1)
+                continue
+            if warm == "serpentine":
+                a_warm = res.x * scales
+            q[coef_idx] = res.x * scales
+            p = target.at(q)
+            conditional = p.potential() - hyperprior_potential(target, q)
+            try:
+                chol = np.linalg.cholesky(p.hessian()[np.ix_(coef_idx, coef_idx)])
+            except np.linalg.LinAlgError:
+                vals.append(float("nan")), stat.append(2)
+                continue
+            logdet = 2.0 * float(np.sum(np.log(np.diagonal(chol))))
+            vals.append(-conditional + 0.5 * n_coef * LN_2PI - 0.5 * logdet
+                        + _inv_gamma_logpdf(c, *prior_c) + _inv_gamma_logpdf(sigma, *prior_s) + log_area)
+            stat.append(0)
+    return np.asarray(vals), np.asarray(stat), np.asarray(nodes)
+
+
+def laplace_grid_combine(values, status, skip_tolerance=0.01):
+    """evidence.py:411-426: skip check, then log-sum-exp of the node values."""
+    skipped = int(np.count_nonzero(status))
+    total = int(status.size)
+    if skipped > skip_tolerance * total:
+        raise RuntimeError(f"grid oracle skipped {skipped}/{total} nodes; result untrustworthy")
+    v = values[status == 0]
+    peak = float(np.max(v))
+    return peak + math.log(float(np.sum(np.exp(v - peak))))

@@ -91,6 +91,13 @@ class ChainConfigC(ctypes.Structure):
                 ("warm_order", ctypes.c_int)]
 
 
+class GridSpecC(ctypes.Structure):
+    _fields_ = [("c_max", ctypes.c_double), ("c_mesh", ctypes.c_double), ("sigma_max", ctypes.c_double),
+                ("sigma_mesh", ctypes.c_double), ("n_pinned", ctypes.c_int),
+                ("pinned_pos", ctypes.c_int * 3), ("pinned_value", ctypes.c_double * 3),
+                ("gtol", ctypes.c_double), ("max_iters", ctypes.c_int), ("memory", ctypes.c_int)]
+
+
 class MoveRecords(ctypes.Structure):
     _fields_ = [("logpost", ctypes.c_void_p), ("h_before", ctypes.c_void_p),
                 ("h_after", ctypes.c_void_p), ("sweeps_mean", ctypes.c_void_p),
@@ -147,6 +154,7 @@ def lib():
         "sgp_version": (ctypes.c_char_p, []),
         "sgp_debug_phase_cycles": (i, [vp, i]),
         "sgp_debug_rotation_check": (i, [ctypes.c_longlong, ctypes.c_ulonglong, vp]),
+        "sgp_laplace_grid": (i, [vp, ctypes.POINTER(GridSpecC), i, vp, vp, vp, vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

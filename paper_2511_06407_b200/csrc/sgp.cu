@@ -18,6 +18,8 @@
 
 extern __shared__ __align__(16) char sgp_smem[];
 
+#include "sgp_grid.cuh"
+
 struct sgp_model {
     ModelDev dev;
     double *d_phi, *d_phis, *d_y, *d_cw, *d_prec, *d_mean;
@@ -945,4 +947,69 @@ extern "C" int sgp_debug_rotation_check(long long n, unsigned long long seed, lo
     h_counts4[2] = (long long)h[2];
     h_counts4[3] = n;
     return SGP_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Laplace-grid evidence oracle (evidence.py:330-426): per-node values on device.
+extern "C" int sgp_laplace_grid(const sgp_model *m, const sgp_grid_spec *spec, int n_nodes, double *h_values,
+                                int *h_status, int *h_iters, void *stream) {
+    if (!m || !spec || !h_values || !h_status || n_nodes < 1) return SGP_EINVAL;
+    const ModelParams &mp = m->dev.mp;
+    if (lg_is_large(m->dev) || mp.hpos[0] < 0 || mp.hpos[1] < 0) return SGP_EINVAL;
+    if (!(spec->c_mesh > 0.0) || !(spec->sigma_mesh > 0.0) || spec->memory < 1 || spec->max_iters < 0) return SGP_EINVAL;
+    GridDev gd{};
+    gd.nc = (int)std::lround(spec->c_max / spec->c_mesh);
+    gd.ns = (int)std::lround(spec->sigma_max / spec->sigma_mesh);
+    if (gd.nc * gd.ns != n_nodes || spec->n_pinned < 0 || spec->n_pinned > 3) return SGP_EINVAL;
+    gd.c_mesh = spec->c_mesh;
+    gd.s_mesh = spec->sigma_mesh;
+    gd.n_pinned = spec->n_pinned;
+    for (int k = 0; k < spec->n_pinned; ++k) {
+        if (spec->pinned_pos[k] < 0 || spec->pinned_pos[k] >= mp.d) return SGP_EINVAL;
+        gd.pin_pos[k] = spec->pinned_pos[k];
+        gd.pin_q[k] = spec->pinned_value[k];
+    }
+    gd.gtol = spec->gtol;
+    gd.max_iters = spec->max_iters;
+    gd.memory = spec->memory;
+    gd.log_area = std::log(spec->c_mesh) + std::log(spec->sigma_mesh);
+    const ChainLaunch L = chain_launch(m);
+    const size_t spc = sgp_scratch_doubles(m);
+    const size_t stride = spc + sgp_grid_scratch_extra(mp.d, spec->memory);
+    int sms = 148;
+    {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const int batch = std::max(1, std::min(n_nodes, sms * L.per_sm * 2));
+    double *d_scr = nullptr, *d_val = nullptr;
+    int *d_st = nullptr, *d_it = nullptr;
+    if (cudaMalloc(&d_scr, stride * batch * sizeof(double)) != cudaSuccess) return SGP_ENOMEM;
+    if (cudaMalloc(&d_val, n_nodes * sizeof(double)) != cudaSuccess || cudaMalloc(&d_st, n_nodes * sizeof(int)) != cudaSuccess ||
+        cudaMalloc(&d_it, n_nodes * sizeof(int)) != cudaSuccess) {
+        cudaFree(d_scr);
+        cudaFree(d_val);
+        cudaFree(d_st);
+        return SGP_ENOMEM;
+    }
+    int rc = launch_prep(k_laplace_grid, L.pl.bytes);
+    for (int node0 = 0; !rc && node0 < n_nodes; node0 += batch) {
+        const int nb = std::min(batch, n_nodes - node0);
+        k_laplace_grid<<<nb, L.nt, L.pl.bytes, S(stream)>>>(m->dev, L.pl, gd, node0, n_nodes, d_scr, spc, stride,
+                                                             d_val, d_st, d_it);
+        rc = check_launch();
+    }
+    if (!rc) {
+        if (cudaMemcpyAsync(h_values, d_val, n_nodes * sizeof(double), cudaMemcpyDeviceToHost, S(stream)) != cudaSuccess ||
+            cudaMemcpyAsync(h_status, d_st, n_nodes * sizeof(int), cudaMemcpyDeviceToHost, S(stream)) != cudaSuccess ||
+            (h_iters && cudaMemcpyAsync(h_iters, d_it, n_nodes * sizeof(int), cudaMemcpyDeviceToHost, S(stream)) != cudaSuccess) ||
+            cudaStreamSynchronize(S(stream)) != cudaSuccess)
+            rc = SGP_ECUDA;
+    }
+    cudaFree(d_scr);
+    cudaFree(d_val);
+    cudaFree(d_st);
+    cudaFree(d_it);
+    return rc;
 }
