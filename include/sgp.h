@@ -232,8 +232,10 @@ int sgp_run_moves(const sgp_model *model, const sgp_chain_config *cfg,
  * (c_g, sigma_g) midpoints is round(c_max/c_mesh) x round(sigma_max/sigma_mesh)
  * nodes in the reference's serpentine order; every node optimises the
  * coefficient block in prior-whitened coordinates with the reference's
- * L-BFGS (memory, strong Wolfe search, gtol, max_iters) from a = 0 and
- * Cholesky-factorises the coefficient Hessian block.  Outputs per node, on the
+ * L-BFGS (memory, strong Wolfe search, gtol, max_iters) from a = 0 (all nodes
+ * concurrently; nodes that fail are retried warm-started from the optimum of
+ * the last converged node before them in serpentine order, the reference's
+ * a_warm) and Cholesky-factorises the coefficient Hessian block.  Outputs per node, on the
  * host: the node log-evidence term (evidence.py:403-410), a status (0 ok,
  * 1 optimiser did not converge, 2 Cholesky failed, 3 objective not finite at
  * the start) and the L-BFGS iteration count.  The caller validates the model

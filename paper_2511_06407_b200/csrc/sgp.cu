@@ -983,22 +983,59 @@ extern "C" int sgp_laplace_grid(const sgp_model *m, const sgp_grid_spec *spec, i
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     }
     const int batch = std::max(1, std::min(n_nodes, sms * L.per_sm * 2));
-    double *d_scr = nullptr, *d_val = nullptr;
-    int *d_st = nullptr, *d_it = nullptr;
+    double *d_scr = nullptr, *d_val = nullptr, *d_aopt = nullptr;
+    int *d_st = nullptr, *d_it = nullptr, *d_list = nullptr;
+    const size_t d = mp.d;
     if (cudaMalloc(&d_scr, stride * batch * sizeof(double)) != cudaSuccess) return SGP_ENOMEM;
     if (cudaMalloc(&d_val, n_nodes * sizeof(double)) != cudaSuccess || cudaMalloc(&d_st, n_nodes * sizeof(int)) != cudaSuccess ||
-        cudaMalloc(&d_it, n_nodes * sizeof(int)) != cudaSuccess) {
+        cudaMalloc(&d_it, n_nodes * sizeof(int)) != cudaSuccess ||
+        cudaMalloc(&d_aopt, (size_t)n_nodes * d * sizeof(double)) != cudaSuccess ||
+        cudaMalloc(&d_list, 2 * (size_t)n_nodes * sizeof(int)) != cudaSuccess) {
         cudaFree(d_scr);
         cudaFree(d_val);
         cudaFree(d_st);
+        cudaFree(d_it);
+        cudaFree(d_aopt);
         return SGP_ENOMEM;
     }
     int rc = launch_prep(k_laplace_grid, L.pl.bytes);
+    // pass 1: every node from a = 0, concurrently
     for (int node0 = 0; !rc && node0 < n_nodes; node0 += batch) {
         const int nb = std::min(batch, n_nodes - node0);
         k_laplace_grid<<<nb, L.nt, L.pl.bytes, S(stream)>>>(m->dev, L.pl, gd, node0, n_nodes, d_scr, spc, stride,
-                                                             d_val, d_st, d_it);
+                                                             d_val, d_st, d_it, nullptr, nullptr, d_aopt);
         rc = check_launch();
+    }
+    // passes 2..: failed nodes again, warm-started from the optimum of the last
+    // converged node before them in serpentine order (the reference's a_warm)
+    std::vector<int> st(n_nodes), list, src;
+    for (int pass = 0; !rc && pass < 4; ++pass) {
+        if (cudaMemcpyAsync(st.data(), d_st, n_nodes * sizeof(int), cudaMemcpyDeviceToHost, S(stream)) != cudaSuccess ||
+            cudaStreamSynchronize(S(stream)) != cudaSuccess) {
+            rc = SGP_ECUDA;
+            break;
+        }
+        list.clear();
+        src.clear();
+        int last = -1;
+        for (int k = 0; k < n_nodes; ++k) {
+            if (st[k] == 0) {
+                last = k;
+            } else if ((st[k] == 1 || st[k] == 2) && last >= 0) {
+                list.push_back(k);
+                src.push_back(last);
+            }
+        }
+        if (list.empty()) break;
+        const int nl = (int)list.size();
+        cudaMemcpyAsync(d_list, list.data(), nl * sizeof(int), cudaMemcpyHostToDevice, S(stream));
+        cudaMemcpyAsync(d_list + n_nodes, src.data(), nl * sizeof(int), cudaMemcpyHostToDevice, S(stream));
+        for (int node0 = 0; !rc && node0 < nl; node0 += batch) {
+            const int nb = std::min(batch, nl - node0);
+            k_laplace_grid<<<nb, L.nt, L.pl.bytes, S(stream)>>>(m->dev, L.pl, gd, node0, nl, d_scr, spc, stride, d_val,
+                                                                 d_st, d_it, d_list, d_list + n_nodes, d_aopt);
+            rc = check_launch();
+        }
     }
     if (!rc) {
         if (cudaMemcpyAsync(h_values, d_val, n_nodes * sizeof(double), cudaMemcpyDeviceToHost, S(stream)) != cudaSuccess ||
@@ -1011,5 +1048,7 @@ extern "C" int sgp_laplace_grid(const sgp_model *m, const sgp_grid_spec *spec, i
     cudaFree(d_val);
     cudaFree(d_st);
     cudaFree(d_it);
+    cudaFree(d_aopt);
+    cudaFree(d_list);
     return rc;
 }

@@ -8,10 +8,11 @@
 // the same CTA-level evaluator the sampler uses; then the Hessian's
 // coefficient block is Cholesky-factorised in the CTA (right-looking, fails
 // exactly where LAPACK dpotrf reports a non-positive pivot) for the log
-// determinant.  Nodes are independent: every node starts at a = 0 instead of
-// the reference's serpentine warm start, which changes the node optimum only
-// within the optimiser tolerance (checked against the oracle's zero-start
-// and serpentine runs in tests/test_gpu_laplace.py).
+// determinant.  Nodes are independent: every node first starts at a = 0
+// instead of the reference's serpentine warm start (same optimum within the
+// optimiser tolerance, tests/test_gpu_laplace.py); nodes that fail from there
+// are retried warm-started from the last converged node before them in
+// serpentine order, which is the reference's own a_warm rule.
 #pragma once
 #include "sgp_chain.cuh"
 
@@ -200,11 +201,18 @@ __device__ __forceinline__ double inv_gamma_logpdf(double th, double a, double b
 
 // status: 0 ok, 1 optimiser did not converge, 2 Cholesky failed, 3 objective not
 // finite at the start (the reference raises ValueError there)
+// list == nullptr: nodes node0 + blockIdx.x (first pass, a = 0 starts);
+// else node = list[node0 + blockIdx.x] warm-started from the optimum of node
+// src[...] (the reference's serpentine a_warm, evidence.py:393-399).  The
+// optimum of every converged node is kept in aopt[node * d + i] (raw coefficients).
 __global__ void __launch_bounds__(SGP_MAX_NT) k_laplace_grid(ModelDev M, SmemPlan pl, GridDev gd, int node0,
                                                             int nodes, double *scratch, size_t spc, size_t stride,
-                                                            double *val, int *status, int *iters) {
-    const int node = node0 + blockIdx.x;
-    if (node >= nodes) return;
+                                                            double *val, int *status, int *iters, const int *list,
+                                                            const int *src, double *aopt) {
+    const int slot_id = node0 + blockIdx.x;
+    if (slot_id >= nodes) return;
+    const int node = list ? list[slot_id] : slot_id;
+    const int from = list ? src[slot_id] : -1;
     const ModelParams &mp = M.mp;
     const int d = mp.d;
     ChainWS w;
@@ -259,7 +267,7 @@ __global__ void __launch_bounds__(SGP_MAX_NT) k_laplace_grid(ModelDev M, SmemPla
     double *hist = my + spc;  // sgp_grid_scratch_extra(d, m) doubles
     double *Sh = hist, *Yh = hist + (size_t)m * d, *rho = hist + (size_t)2 * m * d, *alph = rho + m;
     double *sv = w.bv, *yv = w.tmp;  // candidate pair before acceptance
-    for (int i = threadIdx.x; i < n; i += SGP_NT) x[i] = 0.0;
+    for (int i = threadIdx.x; i < n; i += SGP_NT) x[i] = from >= 0 ? aopt[(size_t)from * d + i] / scl[i] : 0.0;
     __syncthreads();
     int evals = 1, head = 0, cnt = 0, st = 1, it = 0;
     double f = grid_fg(G, x, g);
@@ -327,6 +335,8 @@ __global__ void __launch_bounds__(SGP_MAX_NT) k_laplace_grid(ModelDev M, SmemPla
         if (it == gd.max_iters) st = vmaxabs(g, n, E.red) <= gd.gtol ? 0 : 1;
     }
     double value = NAN;
+    if (st == 0)
+        for (int i = threadIdx.x; i < n; i += SGP_NT) aopt[(size_t)node * d + i] = x[i] * scl[i];
     if (st == 0) {
         // node value at the optimum (evidence.py:400-410)
         for (int i = threadIdx.x; i < n; i += SGP_NT) q[cidx[i]] = x[i] * scl[i];

@@ -343,7 +343,8 @@ def laplace_grid_oracle(model, data, grid_spec=None, *, gtol=1e-6, max_iters=200
     the coefficients (reference evidence.py:330-426).  Nodes run concurrently
     on the device, each from a = 0 (the reference warm-starts along a
     serpentine path; the node optimum is the same to the optimiser
-    tolerance).  Same errors: ValueError for unsuitable models / pinned
+    tolerance); nodes that fail from a = 0 are retried from the last
+    converged node before them in serpentine order (the reference's rule).  Same errors: ValueError for unsuitable models / pinned
     values or a non-finite starting objective, RuntimeError when more than
     ``skip_tolerance`` of the nodes fail."""
     grid = GridSpec() if grid_spec is None else grid_spec
