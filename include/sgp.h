@@ -252,6 +252,15 @@ typedef struct {
 int sgp_laplace_grid(const sgp_model *model, const sgp_grid_spec *spec, int n_nodes, double *h_values,
                      int *h_status, int *h_iters, void *stream);
 
+/* laplace_full (replaces evidence.py:277-304): L-BFGS mode search over all d
+ * coordinates from h_q0 (tempered posterior, tau), Hessian at the mode and its
+ * eigenvalues by the cold cyclic Jacobi (zeta, sweep_cap as
+ * static_eigendecompose).  h_out4 = {ln evidence, U(q*), ln det H, min
+ * eigenvalue}; *h_status 0 ok, 1 mode search did not reach gtol, 2 not positive
+ * definite, 3 objective not finite at the start, 4 Jacobi sweep cap. */
+int sgp_laplace_full(const sgp_model *model, double tau, const double *h_q0, double gtol, int max_iters,
+                     double zeta, int sweep_cap, double *h_out4, int *h_status, int *h_iters, void *stream);
+
 /* Diagnostics: cycles spent by chain 0 in each leapfrog phase (clock64), 16
  * slots: 0 W formation, 1 trace contraction, 2 state + Hessian, 3 MGS,
  * 4 Psi^T H Psi, 5 warm Jacobi, 8 cold Jacobi, 9 whole leapfrog. */

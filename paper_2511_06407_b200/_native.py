@@ -155,6 +155,7 @@ def lib():
         "sgp_debug_phase_cycles": (i, [vp, i]),
         "sgp_debug_rotation_check": (i, [ctypes.c_longlong, ctypes.c_ulonglong, vp]),
         "sgp_laplace_grid": (i, [vp, ctypes.POINTER(GridSpecC), i, vp, vp, vp, vp]),
+        "sgp_laplace_full": (i, [vp, d, vp, d, i, d, i, vp, vp, vp, vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

@@ -1052,3 +1052,42 @@ extern "C" int sgp_laplace_grid(const sgp_model *m, const sgp_grid_spec *spec, i
     cudaFree(d_list);
     return rc;
 }
+
+// laplace_full (evidence.py:277-304) on one posterior: host q0 (d) in,
+// host out[4] = {value, U(q*), log det H, min eigenvalue}, status, iterations.
+extern "C" int sgp_laplace_full(const sgp_model *m, double tau, const double *h_q0, double gtol, int max_iters,
+                                double zeta, int sweep_cap, double *h_out4, int *h_status, int *h_iters, void *stream) {
+    if (!m || !h_q0 || !h_out4 || !h_status || max_iters < 0) return SGP_EINVAL;
+    if (lg_is_large(m->dev)) return SGP_EINVAL;
+    const int d = m->dev.mp.d, memory = 10;
+    SmemPlan pl;
+    chain_plan(m, pl);
+    const size_t spc = sgp_scratch_doubles(m) + sgp_grid_scratch_extra(d, memory);
+    double *buf = nullptr;
+    int *ib = nullptr;
+    if (cudaMalloc(&buf, (spc + d + 4) * sizeof(double)) != cudaSuccess) return SGP_ENOMEM;
+    if (cudaMalloc(&ib, 2 * sizeof(int)) != cudaSuccess) {
+        cudaFree(buf);
+        return SGP_ENOMEM;
+    }
+    double *d_q0 = buf + spc, *d_out = d_q0 + d;
+    int rc = launch_prep(k_laplace_full, pl.bytes);
+    if (!rc && cudaMemcpyAsync(d_q0, h_q0, d * sizeof(double), cudaMemcpyHostToDevice, S(stream)) != cudaSuccess)
+        rc = SGP_ECUDA;
+    if (!rc) {
+        k_laplace_full<<<1, SGP_MAX_NT, pl.bytes, S(stream)>>>(m->dev, pl, d_q0, tau, gtol, max_iters, memory, zeta,
+                                                               sweep_cap, buf, sgp_scratch_doubles(m), d_out, ib,
+                                                               ib + 1);
+        rc = check_launch();
+    }
+    int hb[2] = {0, 0};
+    if (!rc && (cudaMemcpyAsync(h_out4, d_out, 4 * sizeof(double), cudaMemcpyDeviceToHost, S(stream)) != cudaSuccess ||
+                cudaMemcpyAsync(hb, ib, 2 * sizeof(int), cudaMemcpyDeviceToHost, S(stream)) != cudaSuccess ||
+                cudaStreamSynchronize(S(stream)) != cudaSuccess))
+        rc = SGP_ECUDA;
+    *h_status = hb[0];
+    if (h_iters) *h_iters = hb[1];
+    cudaFree(buf);
+    cudaFree(ib);
+    return rc;
+}

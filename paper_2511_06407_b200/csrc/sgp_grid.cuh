@@ -65,7 +65,7 @@ __device__ __forceinline__ double vmaxabs(const double *a, int n, double *red) {
 }
 // out = x + a d
 __device__ __forceinline__ void vaxpy(double *out, const double *x, double a, const double *d, int n) {
-    for (int i = threadIdx.x; i < n; i += SGP_NT) out[i] = x[i] + a * d[i];
+    for (int i = threadIdx.x; i < n; i += SGP_NT) out[i] = __dadd_rn(x[i], __dmul_rn(a, d[i]));  // numpy rounding
     __syncthreads();
 }
 
@@ -146,7 +146,7 @@ __device__ void grid_two_loop(const double *g, double *q, const double *S, const
         const int r = (head + k) % m;
         const double a = rho[r] * vdot(S + (size_t)r * ld, q, n, red);
         if (threadIdx.x == 0) alpha[k] = a;
-        for (int i = threadIdx.x; i < n; i += SGP_NT) q[i] -= a * Y[(size_t)r * ld + i];
+        for (int i = threadIdx.x; i < n; i += SGP_NT) q[i] = __dsub_rn(q[i], __dmul_rn(a, Y[(size_t)r * ld + i]));
         __syncthreads();
     }
     if (cnt > 0) {
@@ -154,14 +154,14 @@ __device__ void grid_two_loop(const double *g, double *q, const double *S, const
         const double sy = vdot(S + (size_t)r * ld, Y + (size_t)r * ld, n, red);
         const double yy = vdot(Y + (size_t)r * ld, Y + (size_t)r * ld, n, red);
         const double f = sy / yy;
-        for (int i = threadIdx.x; i < n; i += SGP_NT) q[i] *= f;
+        for (int i = threadIdx.x; i < n; i += SGP_NT) q[i] = __dmul_rn(q[i], f);
         __syncthreads();
     }
     for (int k = 0; k < cnt; ++k) {
         const int r = (head + k) % m;
         const double b = rho[r] * vdot(Y + (size_t)r * ld, q, n, red);
         const double a = alpha[k];
-        for (int i = threadIdx.x; i < n; i += SGP_NT) q[i] += (a - b) * S[(size_t)r * ld + i];
+        for (int i = threadIdx.x; i < n; i += SGP_NT) q[i] = __dadd_rn(q[i], __dmul_rn(__dsub_rn(a, b), S[(size_t)r * ld + i]));
         __syncthreads();
     }
 }
@@ -193,6 +193,84 @@ __device__ double chol_logdet(double *A, int n, double *red) {
         __syncthreads();
     }
     return fail ? NAN : 2.0 * ld;
+}
+
+// The reference's L-BFGS (lbfgs.py:89-150) on the CTA; x holds the start and
+// returns the iterate, g its gradient, *fout its value.  History rows of
+// stride d in Sh/Yh, ring-ordered.  Returns 0 converged, 1 not converged,
+// 3 objective not finite at the start (lbfgs.py:110 raises ValueError).
+__device__ __noinline__ int grid_lbfgs(GridCtx &G, LsBuf &B, double *x, double *g, double *dir, double *xn,
+                                       double *gn, double *sv, double *yv, double *Sh, double *Yh, double *rho,
+                                       double *alph, int m, double gtol, int max_iters, int *iters, double *fout) {
+    const int n = G.n, d = G.d;
+    int evals = 1, head = 0, cnt = 0, st = 1, it = 0;
+    double f = grid_fg(G, x, g);
+    if (!isfinite(f)) {
+        st = 3;
+    } else {
+        for (it = 0; it < max_iters; ++it) {
+            if (vmaxabs(g, n, G.E->red) <= gtol) {
+                st = 0;
+                break;
+            }
+            grid_two_loop(g, dir, Sh, Yh, rho, m, head, cnt, n, d, alph, G.E->red);
+            for (int i = threadIdx.x; i < n; i += SGP_NT) dir[i] = -dir[i];
+            __syncthreads();
+            if (vdot(g, dir, n, G.E->red) >= 0.0) {
+                cnt = 0;
+                head = 0;
+                for (int i = threadIdx.x; i < n; i += SGP_NT) dir[i] = -g[i];
+                __syncthreads();
+            }
+            double fnew = f;
+            double alpha = grid_wolfe(G, B, x, f, g, dir, 1e-4, 0.9, &fnew, gn, &evals);
+            if (alpha < 0.0 && cnt > 0) {
+                // stale curvature pairs near the optimum: retry once from steepest descent
+                cnt = 0;
+                head = 0;
+                for (int i = threadIdx.x; i < n; i += SGP_NT) dir[i] = -g[i];
+                __syncthreads();
+                alpha = grid_wolfe(G, B, x, f, g, dir, 1e-4, 0.9, &fnew, gn, &evals);
+            }
+            if (alpha < 0.0) {
+                st = vmaxabs(g, n, G.E->red) <= gtol ? 0 : 1;
+                break;
+            }
+            // s = x_new - x, y = g_new - g
+            vaxpy(xn, x, alpha, dir, n);
+            for (int i = threadIdx.x; i < n; i += SGP_NT) {
+                sv[i] = xn[i] - x[i];
+                yv[i] = gn[i] - g[i];
+            }
+            __syncthreads();
+            const double sy = vdot(sv, yv, n, G.E->red);
+            const double ss = vdot(sv, sv, n, G.E->red), yy = vdot(yv, yv, n, G.E->red);
+            if (sy > 1e-12 * sqrt(ss) * sqrt(yy)) {
+                // ring: append at the end, drop the oldest when full (lbfgs.py:140-146)
+                const int slot = (head + cnt) % m;
+                for (int i = threadIdx.x; i < n; i += SGP_NT) {
+                    Sh[(size_t)slot * d + i] = sv[i];
+                    Yh[(size_t)slot * d + i] = yv[i];
+                }
+                if (threadIdx.x == 0) rho[slot] = 1.0 / sy;
+                if (cnt < m)
+                    ++cnt;
+                else
+                    head = (head + 1) % m;
+            }
+            __syncthreads();
+            for (int i = threadIdx.x; i < n; i += SGP_NT) {
+                x[i] = xn[i];
+                g[i] = gn[i];
+            }
+            f = fnew;
+            __syncthreads();
+        }
+        if (it == max_iters) st = vmaxabs(g, n, G.E->red) <= gtol ? 0 : 1;
+    }
+    *iters = it;
+    *fout = f;
+    return st;
 }
 
 __device__ __forceinline__ double inv_gamma_logpdf(double th, double a, double b) {
@@ -269,71 +347,9 @@ __global__ void __launch_bounds__(SGP_MAX_NT) k_laplace_grid(ModelDev M, SmemPla
     double *sv = w.bv, *yv = w.tmp;  // candidate pair before acceptance
     for (int i = threadIdx.x; i < n; i += SGP_NT) x[i] = from >= 0 ? aopt[(size_t)from * d + i] / scl[i] : 0.0;
     __syncthreads();
-    int evals = 1, head = 0, cnt = 0, st = 1, it = 0;
-    double f = grid_fg(G, x, g);
-    if (!isfinite(f)) {
-        st = 3;
-    } else {
-        for (it = 0; it < gd.max_iters; ++it) {
-            if (vmaxabs(g, n, E.red) <= gd.gtol) {
-                st = 0;
-                break;
-            }
-            grid_two_loop(g, dir, Sh, Yh, rho, m, head, cnt, n, d, alph, E.red);
-            for (int i = threadIdx.x; i < n; i += SGP_NT) dir[i] = -dir[i];
-            __syncthreads();
-            if (vdot(g, dir, n, E.red) >= 0.0) {
-                cnt = 0;
-                head = 0;
-                for (int i = threadIdx.x; i < n; i += SGP_NT) dir[i] = -g[i];
-                __syncthreads();
-            }
-            double fnew = f;
-            double alpha = grid_wolfe(G, B, x, f, g, dir, 1e-4, 0.9, &fnew, gn, &evals);
-            if (alpha < 0.0 && cnt > 0) {
-                // stale curvature pairs near the optimum: retry once from steepest descent
-                cnt = 0;
-                head = 0;
-                for (int i = threadIdx.x; i < n; i += SGP_NT) dir[i] = -g[i];
-                __syncthreads();
-                alpha = grid_wolfe(G, B, x, f, g, dir, 1e-4, 0.9, &fnew, gn, &evals);
-            }
-            if (alpha < 0.0) {
-                st = vmaxabs(g, n, E.red) <= gd.gtol ? 0 : 1;
-                break;
-            }
-            // s = x_new - x, y = g_new - g
-            vaxpy(xn, x, alpha, dir, n);
-            for (int i = threadIdx.x; i < n; i += SGP_NT) {
-                sv[i] = xn[i] - x[i];
-                yv[i] = gn[i] - g[i];
-            }
-            __syncthreads();
-            const double sy = vdot(sv, yv, n, E.red);
-            const double ss = vdot(sv, sv, n, E.red), yy = vdot(yv, yv, n, E.red);
-            if (sy > 1e-12 * sqrt(ss) * sqrt(yy)) {
-                // ring: append at the end, drop the oldest when full (lbfgs.py:140-146)
-                const int slot = (head + cnt) % m;
-                for (int i = threadIdx.x; i < n; i += SGP_NT) {
-                    Sh[(size_t)slot * d + i] = sv[i];
-                    Yh[(size_t)slot * d + i] = yv[i];
-                }
-                if (threadIdx.x == 0) rho[slot] = 1.0 / sy;
-                if (cnt < m)
-                    ++cnt;
-                else
-                    head = (head + 1) % m;
-            }
-            __syncthreads();
-            for (int i = threadIdx.x; i < n; i += SGP_NT) {
-                x[i] = xn[i];
-                g[i] = gn[i];
-            }
-            f = fnew;
-            __syncthreads();
-        }
-        if (it == gd.max_iters) st = vmaxabs(g, n, E.red) <= gd.gtol ? 0 : 1;
-    }
+    int it = 0;
+    double f = 0.0;
+    int st = grid_lbfgs(G, B, x, g, dir, xn, gn, sv, yv, Sh, Yh, rho, alph, m, gd.gtol, gd.max_iters, &it, &f);
     double value = NAN;
     if (st == 0)
         for (int i = threadIdx.x; i < n; i += SGP_NT) aopt[(size_t)node * d + i] = x[i] * scl[i];
@@ -376,5 +392,80 @@ __global__ void __launch_bounds__(SGP_MAX_NT) k_laplace_grid(ModelDev M, SmemPla
         val[node] = value;
         status[node] = st;
         iters[node] = it;
+    }
+}
+
+// laplace_full (evidence.py:277-304) for one posterior: L-BFGS over all d
+// coordinates from q0, Hessian at the mode, cold cyclic Jacobi (bit-exact
+// with the reference's Numba sweeps) for the eigenvalues.  out[0] value,
+// out[1] U(q*), out[2] log det, out[3] min eigenvalue; *status 0 ok,
+// 1 mode search did not reach gtol, 2 not positive definite, 3 objective not
+// finite at the start, 4 Jacobi sweep cap (JacobiError); *iters L-BFGS iterations.
+__global__ void __launch_bounds__(SGP_MAX_NT) k_laplace_full(ModelDev M, SmemPlan pl, const double *q0, double tau,
+                                                            double gtol, int max_iters, int memory, double zeta,
+                                                            int sweep_cap, double *scratch, size_t spc, double *out,
+                                                            int *status, int *iters) {
+    const ModelParams &mp = M.mp;
+    const int d = mp.d;
+    ChainWS w;
+    EvalCtx E;
+    setup_ws(w, E, sgp_smem, pl, M, scratch);
+    int *cidx = reinterpret_cast<int *>(w.T);
+    double *scl = w.T + d;
+    for (int i = threadIdx.x; i < d; i += SGP_NT) {
+        cidx[i] = i;
+        scl[i] = 1.0;
+    }
+    double *q = w.q0, *x = w.qc, *g = w.qn, *dir = w.qs, *xn = w.p, *gn = w.ph;
+    for (int i = threadIdx.x; i < d; i += SGP_NT) x[i] = q0[i];
+    __syncthreads();
+    GridCtx G{&w, &E, cidx, scl, q, tau, d, d};
+    LsBuf B{w.pn, w.v0, w.tv};
+    double *hist = scratch + spc;
+    double *Sh = hist, *Yh = hist + (size_t)memory * d, *rho = hist + (size_t)2 * memory * d, *alph = rho + memory;
+    int it = 0;
+    double f = 0.0;
+    int st = grid_lbfgs(G, B, x, g, dir, xn, gn, w.bv, w.tmp, Sh, Yh, rho, alph, memory, gtol, max_iters, &it, &f);
+    double ld = 0.0, lmin = NAN, value = NAN;
+    if (st == 0) {
+        for (int i = threadIdx.x; i < d; i += SGP_NT) q[i] = x[i];
+        __syncthreads();
+        EvalOut o;
+        eval_state(E, q, tau, SGP_EVAL_HESSIAN, w.grad, w.H, o);
+        if (*E.status) {
+            st = 2;
+        } else {
+            sgp_chain_config cfg{};
+            cfg.zeta = zeta;
+            cfg.sweep_cap = sweep_cap;
+            cfg.kappa = 1.0;
+            int sw = 0;
+            if (eig_cold(w, E, d, cfg, 0, &sw)) {
+                st = 4;
+            } else {
+                double s = 0.0, mn = INFINITY;
+                for (int j = threadIdx.x; j < d; j += SGP_NT) {
+                    mn = fmin(mn, w.lam[0][j]);
+                    s += log(w.lam[0][j]);
+                }
+                mn = -block_max_nan(-mn, E.red);
+                s = block_sum(s, E.red);
+                lmin = mn;
+                if (!(mn > 0.0)) {
+                    st = 2;
+                } else {
+                    ld = s;
+                    value = -f + 0.5 * d * SGP_LN_2PI - 0.5 * ld;
+                }
+            }
+        }
+    }
+    if (threadIdx.x == 0) {
+        out[0] = value;
+        out[1] = f;
+        out[2] = ld;
+        out[3] = lmin;
+        *status = st;
+        *iters = it;
     }
 }

@@ -76,3 +76,16 @@ def test_unsolvable_nodes_poison_the_result():
     grid = GridSpec(c_max=0.5, c_mesh=0.25, sigma_max=0.5, sigma_mesh=0.25, pinned=(("c_l", 1.0),))
     with pytest.raises(RuntimeError, match="grid oracle skipped"):
         laplace_grid_oracle(free, data, grid, gtol=1e-15, max_iters=1)
+
+
+def test_laplace_full_matches_reference():
+    """evidence.py:277-304 on the device: mode search + cold Jacobi log-determinant."""
+    from paper_2511_06407_b200.evidence import laplace_full
+
+    x, y = G["conj_x"], G["conj_y"]
+    data = rrgp.Dataset(x, y)
+    fixed = rrgp.build_model("nl-mean", x, feature_count=8, intercept_variance=1e-4,
+                             fixed_hypers={"c_g": 1.3, "sigma_g": 2.1, "c_l": 1.0})
+    assert abs(laplace_full(fixed, data) - float(G["laplace_full_fixed"])) < 1e-8
+    ld, lm = logi()
+    assert abs(laplace_full(lm, ld) - float(G["laplace_full_logi"])) < 1e-8
