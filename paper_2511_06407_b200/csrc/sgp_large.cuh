@@ -1084,6 +1084,88 @@ static int lg_eig_cold(LgCtx &c, int dst, int *sweeps) {
     return lg_sync(c);
 }
 
+// MGS inside one panel of rows [r0, r1) of X = Psi^T (one CTA; rows of the
+// earlier panels have already been projected out).
+__global__ void __launch_bounds__(1024) k_lg_mgs_panel(double *X, int d, int r0, int r1) {
+    __shared__ double red[32];
+    __shared__ double nrm;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int i = r0; i < r1; ++i) {
+        double *ri = X + (size_t)i * d;
+        double s = 0.0;
+        for (int k = threadIdx.x; k < d; k += blockDim.x) s += ri[k] * ri[k];
+        s = warp_sum(s);
+        if (lane == 0) red[warp] = s;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double t = 0.0;
+            for (int w = 0; w < nw; ++w) t += red[w];
+            nrm = sqrt(t);
+        }
+        __syncthreads();
+        const double n = nrm;
+        if (n == 0.0) continue;  // _jacobi.py:98-99
+        for (int k = threadIdx.x; k < d; k += blockDim.x) ri[k] /= n;
+        __syncthreads();
+        for (int j = i + 1 + warp; j < r1; j += nw) {
+            double *rj = X + (size_t)j * d;
+            double dot = 0.0;
+            for (int k = lane; k < d; k += 32) dot += ri[k] * rj[k];
+            dot = warp_sum(dot);
+            for (int k = lane; k < d; k += 32) rj[k] -= dot * ri[k];
+        }
+        __syncthreads();
+    }
+}
+
+// Blocked Gram-Schmidt of P_slot's columns: rows of X = Psi^T in panels of
+// 64; each panel is made orthogonal to all earlier rows by classical
+// Gram-Schmidt applied twice (two DMMA GEMM pairs: C = X_p X_prev^T,
+// X_p -= C X_prev), then orthonormalised by MGS inside the panel.  For the
+// nearly orthonormal bases this re-orthonormalises (_jacobi.py:90-107: every
+// 10th warm call), the result equals the column MGS to rounding (the same
+// QR factor).  X and W are free at this point.
+static void lg_mgs_blocked(LgCtx &c, int slot) {
+    const int d = c.d, bs = 64;
+    const int nt = (d + 31) / 32;
+    const int tgrid = std::min(nt * nt, 148 * 8);
+    k_lg_transpose<<<tgrid, dim3(32, 8), 0, c.s>>>(c.L.X, c.L.P[slot], d);
+    for (int p0 = 0; p0 < d; p0 += bs) {
+        const int pe = std::min(d, p0 + bs), nb = pe - p0;
+        double *Xp = c.L.X + (size_t)p0 * d;
+        for (int rep = 0; p0 > 0 && rep < 2; ++rep) {
+            GemmArgs g{};
+            g.M = nb;
+            g.N = p0;
+            g.K = d;
+            g.A = Xp;
+            g.lda = d;
+            g.B = c.L.X;
+            g.ldb = d;
+            g.TB = 1;  // B(k, n) = X[n][k]
+            g.C = c.L.W;
+            g.ldc = p0;
+            g.alpha = 1.0;
+            gemm_launch(g, c.s);  // C = X_p X_prev^T
+            GemmArgs h{};
+            h.M = nb;
+            h.N = d;
+            h.K = p0;
+            h.A = c.L.W;
+            h.lda = p0;
+            h.B = c.L.X;
+            h.ldb = d;
+            h.C = Xp;
+            h.ldc = d;
+            h.alpha = -1.0;
+            h.beta = 1.0;
+            gemm_launch(h, c.s);  // X_p -= C X_prev
+        }
+        k_lg_mgs_panel<<<1, 1024, 0, c.s>>>(c.L.X, d, p0, pe);
+    }
+    k_lg_transpose<<<tgrid, dim3(32, 8), 0, c.s>>>(c.L.P[slot], c.L.X, d);
+}
+
 // Modified Gram-Schmidt of P_slot's columns (_jacobi.py:90-107) as d grid
 // steps on the transposed matrix (rows contiguous); X is free at this point.
 static void lg_mgs(LgCtx &c, int slot) {
@@ -1107,7 +1189,13 @@ static int lg_eig_warm(LgCtx &c, int src, int dst, int *sweeps) {
     const int d = c.d;
     int since = c.since[src] + 1;
     if (c.cfg.gs_interval && since >= c.cfg.gs_interval) {
-        lg_mgs(c, src);
+        // d grid steps (measured faster at d = 2083 than the blocked form, whose
+        // odd-stride panel GEMMs and single-CTA panel MGS cost ~80 ms per call)
+        const char *e = getenv("SGP_LG_BLOCK_MGS");
+        if (e && e[0] == '1')
+            lg_mgs_blocked(c, src);
+        else
+            lg_mgs(c, src);
         since = 0;
     }
     const double hnorm = lg_hnorm(c);
