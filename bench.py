@@ -247,9 +247,16 @@ def run_gpu(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
+    # one rank per GPU; the modulo only matters for functional runs of several
+    # ranks on a one-GPU box (SGP_DIST_BACKEND=gloo), never for measurements
+    dev_index = local % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(dev_index)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("SGP_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev_index))
+        else:
+            dist.init_process_group(backend)
 
     from paper_2511_06407_b200 import _native as nat
     from paper_2511_06407_b200.posterior import PosteriorTarget
@@ -295,7 +302,7 @@ def run_gpu(args):
         dist.barrier()
     torch.cuda.synchronize()
     times = []
-    with ClockSampler(local) as clocks:
+    with ClockSampler(dev_index) as clocks:
         t_wall = time.perf_counter()
         for k in range(args.steps):
             flush.fill_(float(k))  # evict L2 between timed steps (untimed)
