@@ -31,8 +31,10 @@ struct SmemPlan {
 
 __host__ __device__ inline size_t sgp_round2(size_t x) { return (x + 1) & ~size_t(1); }
 
-__host__ __device__ inline size_t sgp_stage_doubles(int Dp, int CH) {
-    return sgp_round2(2 * ((size_t)CH * (Dp + 2) + 3 * (size_t)CH) + 2 * (size_t)(Dp / 4) * CH * 3 + 2);
+// double-buffered Phi / weight stage + the trace's per-tile partial sums
+__host__ __device__ inline size_t sgp_stage_doubles(int Dp, int CH, int nt) {
+    return sgp_round2(2 * ((size_t)CH * (Dp + 2) + 3 * (size_t)CH) +
+                      (size_t)sgp_trace_ks(Dp, CH, nt) * (Dp / 4) * CH * 3 + 2);
 }
 
 __host__ __device__ inline size_t sgp_mat_doubles(int i, int d, int Dp) {
@@ -42,6 +44,13 @@ __host__ __device__ inline size_t sgp_mat_doubles(int i, int d, int Dp) {
 __host__ __device__ inline SmemPlan sgp_smem_plan(int d, int Dp, int nt, size_t budget, int ch = 0) {
     SmemPlan s;
     s.CH = ch > 0 ? ch : (nt <= 64 ? 16 : ((Dp <= 48 && nt >= 128) ? 64 : 32));
+    // smaller sample chunks when the fixed part alone would exceed the per-CTA budget
+    // (keeps two 256-thread CTAs per SM at d ~ 160)
+    auto fixed_bytes = [&](int CH) {
+        return (128 + sgp_round2(16 * (size_t)d + 8) + sgp_round2(6 * (size_t)((d + 2) / 2) + 8) +
+                sgp_stage_doubles(Dp, CH, nt)) * sizeof(double);
+    };
+    while (ch <= 0 && s.CH > 16 && fixed_bytes(s.CH) > budget) s.CH >>= 1;
     size_t off = 0;
     off += 128 * sizeof(double);  // red + status + scalars + ints
     s.off_vec = off;
@@ -49,7 +58,7 @@ __host__ __device__ inline SmemPlan sgp_smem_plan(int d, int Dp, int nt, size_t 
     s.off_prm = off;
     off += sgp_round2(6 * (size_t)((d + 2) / 2) + 8) * sizeof(double);
     s.off_stage = off;
-    off += sgp_stage_doubles(Dp, s.CH) * sizeof(double);
+    off += sgp_stage_doubles(Dp, s.CH, nt) * sizeof(double);
     for (int i = 0; i < SGP_NMAT; ++i) {
         const size_t m = sgp_round2(sgp_mat_doubles(i, d, Dp)) * sizeof(double);
         // Wp (padded trace operand) shares H's slot: H is consumed by the
@@ -61,7 +70,7 @@ __host__ __device__ inline SmemPlan sgp_smem_plan(int d, int Dp, int nt, size_t 
         }
         // X (product scratch of the W formation and Psi^T H Psi) shares the
         // tile stage, which is idle in both
-        if (i == 5 && (size_t)d * d <= sgp_stage_doubles(Dp, s.CH)) {
+        if (i == 5 && (size_t)d * d <= sgp_stage_doubles(Dp, s.CH, nt)) {
             s.off_mat[5] = s.off_stage;
             continue;
         }
@@ -117,7 +126,7 @@ __device__ inline void setup_ws(ChainWS &w, EvalCtx &E, char *smem, const SmemPl
 // conflict-free (shared): the tile stage when it fits (idle during the
 // Jacobi), else the X scratch matrix (free between Psi^T H Psi and the next W).
 __device__ __forceinline__ double *jac_vwork(const ChainWS &w, const EvalCtx &E, int d) {
-    if (E.stage && (size_t)d * d <= sgp_stage_doubles(E.M.mp.Dp, E.CH)) return E.stage;
+    if (E.stage && (size_t)d * d <= sgp_stage_doubles(E.M.mp.Dp, E.CH, SGP_NT)) return E.stage;
     return w.X;
 }
 // Vt (column-major) -> P (row-major)

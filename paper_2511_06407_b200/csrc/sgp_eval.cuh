@@ -4,6 +4,10 @@
 #pragma once
 #include "sgp_core.cuh"
 
+// trace K-split factor (trace_lik_tiled): two threads per tile when there are
+// at most half as many 4x4 tiles as threads (the stage sizing uses the same rule)
+__host__ __device__ inline int sgp_trace_ks(int Dp, int CH, int nt) { return 2 * (CH / 4) * (Dp / 4) <= nt ? 2 : 1; }
+
 struct EvalCtx {
     ModelDev M;
     double *S;      // per-sample fields, F_COUNT x ld (global scratch)
@@ -251,7 +255,7 @@ __device__ __noinline__ void trace_lik_tiled(EvalCtx &E, const double *Wp) {
     const int ngrp = CH >> 2, tiles = ngrp * nb;
     // K split: with fewer tiles than threads, ks threads share a tile, each
     // over a slice of the contraction index; their row-dot partials add.
-    const int ks = (2 * tiles <= SGP_NT) ? 2 : 1;
+    const int ks = sgp_trace_ks(Dp, CH, SGP_NT);  // must match the stage sizing (sgp_stage_doubles)
     double *part = stage_buf(E, 2);  // ks * nb * CH * 3, after the two stage buffers
     __syncthreads();
     stage_issue(E, 0, 0, 0, 0);
