@@ -338,7 +338,7 @@ static ChainLaunch chain_launch(const sgp_model *m) {
     const char *ech = getenv("SGP_STAGE_CH");
     const int ch = ech ? atoi(ech) : 0;
     const size_t budget = (227 * 1024) / L.per_sm - 1024;
-    L.pl = sgp_smem_plan(m->dev.mp.d, m->dev.mp.Dp, nt, budget, (ch == 16 || ch == 32 || ch == 64) ? ch : 0);
+    L.pl = sgp_smem_plan(m->dev.mp.d, m->dev.mp.Dp, nt, budget, (ch == 8 || ch == 16 || ch == 32 || ch == 64) ? ch : 0);
     return L;
 }
 

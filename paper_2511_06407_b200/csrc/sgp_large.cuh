@@ -599,43 +599,89 @@ __global__ void __launch_bounds__(BJ_SOLVE_NT) k_bj_solve(const double *A, int d
                 rp[tid] = p;
                 rq[tid] = q;
                 ract[tid] = act;
-                if (act) {
+                const unsigned bal = __ballot_sync(0xffffffffu, act);
+                if (tid == 0 && bal) {
                     any = 1;
-                    atomicAdd(&nrot, 1);
+                    nrot += __popc(bal);
                 }
             }
             __syncthreads();
-            // rows p, q
-            for (int it = tid; it < np * m; it += blockDim.x) {
-                const int kk = it / m, l = it - kk * m;
-                if (!ract[kk]) continue;
-                const int p = rp[kk], q = rq[kk];
-                const double c = rc[kk], sn = rs[kk];
-                const double ap = S[p][l], aq = S[q][l];
-                S[p][l] = c * ap - sn * aq;
-                S[q][l] = sn * ap + c * aq;
+            // fused two-sided update: thread (P, Q) owns the 2x2 block rows {p_P, q_P} x
+            // cols {p_Q, q_Q}; row rotation P then column rotation Q, in registers
+            // (the same rounded operations as a row pass followed by a column pass)
+            double nv[4], nu[2][2];
+            int bi[2], bj[2], ui[2];
+            bool act_blk = false, act_u[2] = {false, false};
+            if (tid < np * np) {
+                const int P = tid / np, Q = tid - P * np;
+                const bool aP = ract[P], aQ = ract[Q];
+                act_blk = aP || aQ;
+                const int p1 = rp[P], q1 = rq[P], p2 = rp[Q], q2 = rq[Q];
+                bi[0] = p1;
+                bi[1] = q1;
+                bj[0] = p2;
+                bj[1] = q2;
+                if (act_blk) {
+                    if (P == Q) {
+                        nv[0] = rpp[P] - rt[P];
+                        nv[1] = 0.0;
+                        nv[2] = 0.0;
+                        nv[3] = rqq[P] + rt[P];
+                    } else {
+                        const double cP = rc[P], sP = rs[P], cQ = rc[Q], sQ = rs[Q];
+                        const double a00 = S[p1][p2], a01 = S[p1][q2], a10 = S[q1][p2], a11 = S[q1][q2];
+                        double r00 = a00, r01 = a01, r10 = a10, r11 = a11;
+                        if (aP) {
+                            r00 = cP * a00 - sP * a10;
+                            r10 = sP * a00 + cP * a10;
+                            r01 = cP * a01 - sP * a11;
+                            r11 = sP * a01 + cP * a11;
+                        }
+                        if (aQ) {
+                            nv[0] = cQ * r00 - sQ * r01;
+                            nv[1] = sQ * r00 + cQ * r01;
+                            nv[2] = cQ * r10 - sQ * r11;
+                            nv[3] = sQ * r10 + cQ * r11;
+                        } else {
+                            nv[0] = r00;
+                            nv[1] = r01;
+                            nv[2] = r10;
+                            nv[3] = r11;
+                        }
+                    }
+                }
+            }
+            // columns p, q of U for two (row, pair) items per thread
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int it = tid + h * blockDim.x;
+                if (it < np * m) {
+                    const int l = it / np, kk = it - l * np;
+                    ui[h] = it;
+                    if (ract[kk]) {
+                        act_u[h] = true;
+                        const int p = rp[kk], q = rq[kk];
+                        const double c = rc[kk], sn = rs[kk];
+                        const double up = U[l][p], uq = U[l][q];
+                        nu[h][0] = c * up - sn * uq;
+                        nu[h][1] = sn * up + c * uq;
+                    }
+                }
             }
             __syncthreads();
-            // columns p, q of S and U
-            for (int it = tid; it < np * m; it += blockDim.x) {
-                const int l = it / np, kk = it - l * np;
-                if (!ract[kk]) continue;
-                const int p = rp[kk], q = rq[kk];
-                const double c = rc[kk], sn = rs[kk];
-                const double ap = S[l][p], aq = S[l][q];
-                S[l][p] = c * ap - sn * aq;
-                S[l][q] = sn * ap + c * aq;
-                const double up = U[l][p], uq = U[l][q];
-                U[l][p] = c * up - sn * uq;
-                U[l][q] = sn * up + c * uq;
+            if (act_blk) {
+                S[bi[0]][bj[0]] = nv[0];
+                S[bi[0]][bj[1]] = nv[1];
+                S[bi[1]][bj[0]] = nv[2];
+                S[bi[1]][bj[1]] = nv[3];
             }
-            __syncthreads();
-            if (tid < np && ract[tid]) {
-                const int p = rp[tid], q = rq[tid];
-                S[p][q] = 0.0;
-                S[q][p] = 0.0;
-                S[p][p] = rpp[tid] - rt[tid];
-                S[q][q] = rqq[tid] + rt[tid];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                if (act_u[h]) {
+                    const int l = ui[h] / np, kk = ui[h] - l * np;
+                    U[l][rp[kk]] = nu[h][0];
+                    U[l][rq[kk]] = nu[h][1];
+                }
             }
             __syncthreads();
         }
