@@ -67,11 +67,9 @@ __device__ inline void lg_setup(ChainWS &w, EvalCtx &E, const LgPtrs &L, char *s
 enum LgOp {
     LG_STATE = 0,      // eval_state(q = vec[a0], what = i0): pot -> sc[2], sumpot -> sc[3]
     LG_TRACE = 1,      // t -> tv from S (c^(j) precomputed) at q = vec[a0]
-    LG_BVEC = 2,       // bv = Psi_slot^T p(vec[a0]) / g_slot
-    LG_APPLY = 3,      // vec[a1] = metric_apply(P_slot, g_slot, vec[a0], mode i0)
+    // 2, 3: (Psi^T v, G^-1 v) now grid kernels, lg_tvec / lg_apply_g
     LG_GLAM = 4,       // lam_slot = diag(H); g_slot, logdet -> sc[slot]; since -> si[slot] = i0
-    LG_MGS = 5,        // mgs(P_slot)
-    LG_KINETIC = 6,    // sc[6] = kinetic(p, slot)
+    // 5, 6: (MGS, kinetic) now grid kernels, lg_mgs / k_lg_kinetic_fin
     LG_COLD = 7,       // cold cyclic Jacobi of H into P_slot (bit-exact reference order)
     LG_OFFNORM = 8,    // sc[7] = off-norm of H (full storage)
     LG_LOADFRAME = 9,  // P_0 <- psi, lam_0 <- lam (from chain state), since
@@ -106,13 +104,6 @@ __global__ void __launch_bounds__(LG_NT) k_lg_op(LgPtrs L, LgOpArgs a) {
         case LG_TRACE:
             eval_trace(E, V + (size_t)a.a0 * d, a.tau, w.W, w.tv);
             break;
-        case LG_BVEC:
-            mat_tvec(w.bv, w.P[a.slot], V + (size_t)a.a0 * d, d);
-            for (int j = threadIdx.x; j < d; j += SGP_NT) w.bv[j] /= w.g[a.slot][j];
-            break;
-        case LG_APPLY:
-            metric_apply(V + (size_t)a.a1 * d, w.bv, w.P[a.slot], w.g[a.slot], V + (size_t)a.a0 * d, d, a.i0);
-            break;
         case LG_GLAM: {
             for (int j = threadIdx.x; j < d; j += SGP_NT) w.lam[a.slot][j] = w.H[(size_t)j * d + j];
             __syncthreads();
@@ -121,14 +112,6 @@ __global__ void __launch_bounds__(LG_NT) k_lg_op(LgPtrs L, LgOpArgs a) {
                 w.sc[a.slot] = ld;
                 w.si[a.slot] = a.i0;
             }
-            break;
-        }
-        case LG_MGS:
-            mgs(w.P[a.slot], d, E.red);
-            break;
-        case LG_KINETIC: {
-            const double qd = metric_quad(w.tmp, w.P[a.slot], w.g[a.slot], w.p, d, E.red);
-            if (threadIdx.x == 0) w.sc[6] = 0.5 * qd + 0.5 * (d * SGP_LN_2PI + w.sc[a.slot]);
             break;
         }
         case LG_COLD: {
