@@ -26,6 +26,7 @@ struct ChainWS {
 struct SmemPlan {
     int CH;
     size_t off_vec, off_prm, off_stage, bytes;
+    size_t stage_cap;  // doubles in the stage region (>= sgp_stage_doubles)
     size_t off_mat[SGP_NMAT];  // byte offset in smem, or (size_t)-1 if in scratch
 };
 
@@ -58,7 +59,17 @@ __host__ __device__ inline SmemPlan sgp_smem_plan(int d, int Dp, int nt, size_t 
     s.off_prm = off;
     off += sgp_round2(6 * (size_t)((d + 2) / 2) + 8) * sizeof(double);
     s.off_stage = off;
-    off += sgp_stage_doubles(Dp, s.CH, nt) * sizeof(double);
+    s.stage_cap = sgp_stage_doubles(Dp, s.CH, nt);
+    {
+        // CTAs without V-update overlap keep the eigenvector working copy and one
+        // rotation-log slot in the stage during a Jacobi: grow the stage to hold
+        // both when that still leaves room for H (the Jacobi matrix)
+        const size_t need = sgp_round2((size_t)d * d) + sgp_jlog_slot(d);
+        const size_t hdd = sgp_round2((size_t)d * d) * sizeof(double);
+        if (nt <= 64 && d <= 256 && need > s.stage_cap && off + need * sizeof(double) + hdd <= budget)
+            s.stage_cap = sgp_round2(need);
+    }
+    off += s.stage_cap * sizeof(double);
     for (int i = 0; i < SGP_NMAT; ++i) {
         const size_t m = sgp_round2(sgp_mat_doubles(i, d, Dp)) * sizeof(double);
         // Wp (padded trace operand) shares H's slot: H is consumed by the
@@ -70,7 +81,7 @@ __host__ __device__ inline SmemPlan sgp_smem_plan(int d, int Dp, int nt, size_t 
         }
         // X (product scratch of the W formation and Psi^T H Psi) shares the
         // tile stage, which is idle in both
-        if (i == 5 && (size_t)d * d <= sgp_stage_doubles(Dp, s.CH, nt)) {
+        if (i == 5 && (size_t)d * d <= s.stage_cap) {
             s.off_mat[5] = s.off_stage;
             continue;
         }
@@ -110,6 +121,7 @@ __device__ inline void setup_ws(ChainWS &w, EvalCtx &E, char *smem, const SmemPl
     w.prm = reinterpret_cast<double *>(smem + pl.off_prm);
     E.stage = reinterpret_cast<double *>(smem + pl.off_stage);
     E.CH = pl.CH;
+    E.stage_cap = (int)pl.stage_cap;
     E.S = scratch;
     E.ext_trace = 0;
     double **mats[SGP_NMAT] = {&w.H, &E.wp, &w.W, &w.P[0], &w.P[1], &w.X, &w.T};
@@ -126,8 +138,14 @@ __device__ inline void setup_ws(ChainWS &w, EvalCtx &E, char *smem, const SmemPl
 // conflict-free (shared): the tile stage when it fits (idle during the
 // Jacobi), else the X scratch matrix (free between Psi^T H Psi and the next W).
 __device__ __forceinline__ double *jac_vwork(const ChainWS &w, const EvalCtx &E, int d) {
-    if (E.stage && (size_t)d * d <= sgp_stage_doubles(E.M.mp.Dp, E.CH, SGP_NT)) return E.stage;
+    if (E.stage && (size_t)d * d <= (size_t)E.stage_cap) return E.stage;
     return w.X;
+}
+// one rotation-log slot after the V working copy in the stage, when both fit
+__device__ __forceinline__ double *jac_log_smem(const EvalCtx &E, const double *Vt, int d) {
+    if (Vt != E.stage) return nullptr;
+    const size_t off = sgp_round2((size_t)d * d);
+    return off + sgp_jlog_slot(d) <= (size_t)E.stage_cap ? E.stage + off : nullptr;
 }
 // Vt (column-major) -> P (row-major)
 __device__ __forceinline__ void jac_vwork_out(double *P, const double *Vt, int d) {
@@ -156,7 +174,7 @@ __device__ __noinline__ int eig_cold(ChainWS &w, EvalCtx &E, int d, const sgp_ch
     int sw;
     {
         SGP_PROF(8);
-        sw = jacobi_cyclic(w.H, Vt, d, tol, skip, cfg.sweep_cap, E.red, w.jlog, 1, d);
+        sw = jacobi_cyclic(w.H, Vt, d, tol, skip, cfg.sweep_cap, E.red, w.jlog, 1, d, jac_log_smem(E, Vt, d));
     }
     jac_vwork_out(w.P[dst], Vt, d);
     if (sweeps_out) *sweeps_out = sw;
@@ -201,7 +219,7 @@ __device__ __noinline__ int eig_warm(ChainWS &w, EvalCtx &E, int d, const sgp_ch
             Vt[idx] = w.P[src][k * d + j];
         }
         __syncthreads();
-        sw = jacobi_cyclic(w.H, Vt, d, tol, skip, cfg.sweep_cap, E.red, w.jlog, 1, d);
+        sw = jacobi_cyclic(w.H, Vt, d, tol, skip, cfg.sweep_cap, E.red, w.jlog, 1, d, jac_log_smem(E, Vt, d));
         jac_vwork_out(w.P[dst], Vt, d);
     } else {
         mat_copy(w.P[dst], w.P[src], d * d);

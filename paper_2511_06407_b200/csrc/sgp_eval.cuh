@@ -16,6 +16,7 @@ struct EvalCtx {
     int ext_trace;  // large-d path: 1 = c^(j) already in S; 2 = t[0, Dtot) already holds the likelihood part
     double su_ext;  // large-d path: sum_i U_i computed by a grid reduction
     int CH;         // samples per chunk
+    int stage_cap;  // doubles available in the stage region
     double *red;    // smem reduction scratch (>= 64 doubles)
     int *status;    // smem status word
 };

@@ -46,6 +46,7 @@ __device__ inline void lg_setup(ChainWS &w, EvalCtx &E, const LgPtrs &L, char *s
     E.stage = nullptr;
     E.wp = nullptr;
     E.CH = 32;
+    E.stage_cap = 0;
     E.ext_trace = 2;
     E.su_ext = 0.0;
     w.sc = L.sc;
