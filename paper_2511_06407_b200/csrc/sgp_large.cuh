@@ -819,7 +819,9 @@ static void bj_build_desc(const LgPtrs &L, std::vector<GemmArgs> &out) {
             for (int k = 0; k < np; ++k) {
                 int I, J;
                 bj_pair(r, k, nbk, I, J);
-                const double *Uk = L.bjU + (size_t)k * BJ_N * BJ_N;
+                // U of round r lives in buffer r & 1 (the V update of round r may still be
+                // reading it while round r + 1 is being solved on the other stream)
+                const double *Uk = L.bjU + ((size_t)(r & 1) * np + k) * BJ_N * BJ_N;
                 GemmArgs g{};
                 g.alpha = 1.0;
                 g.beta = 0.0;
@@ -1039,8 +1041,26 @@ static int lg_jacobi_block(LgCtx &c, int dst, double tol, double skip, int *swee
         if (e && atoi(e) > 0) inner_cap = atoi(e);
         configured = true;
     }
+    // Two streams per round: the A chain (pair solve -> column update -> row update -> fix)
+    // runs on a high-priority stream; the eigenvector update V' = V U, which nothing in the
+    // chain reads, runs on the caller's stream and overlaps the next round's pair solve
+    // (np CTAs, a fraction of the SMs).  U is double-buffered by round parity.
+    static cudaStream_t hs = nullptr;
+    static cudaEvent_t ev_in, ev_solved, ev_chain, ev_v[2];
+    static bool overlap = true;
+    if (!hs) {
+        int lo = 0, hi = 0;
+        cudaDeviceGetStreamPriorityRange(&lo, &hi);
+        cudaStreamCreateWithPriority(&hs, cudaStreamNonBlocking, hi);
+        for (cudaEvent_t *e : {&ev_in, &ev_solved, &ev_chain, &ev_v[0], &ev_v[1]})
+            cudaEventCreateWithFlags(e, cudaEventDisableTiming);
+        const char *e = getenv("SGP_BJ_OVERLAP");  // 0: everything on the caller's stream (A/B timing)
+        overlap = !(e && e[0] == '0');
+    }
+    cudaStream_t as = overlap ? hs : c.s;
     int vcur = 0, sw = 0;
     const size_t per_round = (size_t)4 * np;
+    const size_t ubuf = (size_t)np * BJ_N * BJ_N;
     const int nb_part = 148 * 2;
     for (;;) {
         k_bj_offnorm<<<nb_part, 256, 0, c.s>>>(c.L.bjA, dp, c.L.bjPart);
@@ -1051,15 +1071,30 @@ static int lg_jacobi_block(LgCtx &c, int dst, double tol, double skip, int *swee
             *sweeps = -1;
             return SGP_STATUS_JACOBI;
         }
+        if (overlap) {
+            cudaEventRecord(ev_in, c.s);
+            cudaStreamWaitEvent(hs, ev_in, 0);
+        }
         for (int r = 0; r < nbk - 1; ++r) {
             const GemmArgs *D = c.L.bjDesc + (size_t)r * per_round;
-            k_bj_solve<<<np, BJ_SOLVE_NT, BJ_SMEM, c.s>>>(c.L.bjA, dp, r, nbk, skip, c.L.bjU, c.L.bjLam, c.L.bjCnt,
-                                                  inner_cap);
-            gemm_launch_batched<0, 0>(D, np, dp, BJ_N, c.s);                            // T = A U (columns)
-            gemm_launch_batched<1, 0>(D + np, np, BJ_N, dp, c.s);                       // A = U^T T (rows)
+            double *Ur = c.L.bjU + (size_t)(r & 1) * ubuf;
+            if (overlap) cudaStreamWaitEvent(hs, ev_v[r & 1], 0);  // V update of round r - 2 read Ur
+            k_bj_solve<<<np, BJ_SOLVE_NT, BJ_SMEM, as>>>(c.L.bjA, dp, r, nbk, skip, Ur, c.L.bjLam, c.L.bjCnt,
+                                                     inner_cap);
+            if (overlap) {
+                cudaEventRecord(ev_solved, hs);
+                cudaStreamWaitEvent(c.s, ev_solved, 0);
+            }
+            gemm_launch_batched<0, 0>(D, np, dp, BJ_N, as);                              // T = A U (columns)
+            gemm_launch_batched<1, 0>(D + np, np, BJ_N, dp, as);                         // A = U^T T (rows)
             gemm_launch_batched<0, 0>(D + (size_t)(vcur ? 3 : 2) * np, np, dp, BJ_N, c.s);  // V' = V U
-            k_bj_fix<<<np, 256, 0, c.s>>>(c.L.bjA, dp, r, nbk, c.L.bjLam, c.L.bjCnt);
+            if (overlap) cudaEventRecord(ev_v[r & 1], c.s);
+            k_bj_fix<<<np, 256, 0, as>>>(c.L.bjA, dp, r, nbk, c.L.bjLam, c.L.bjCnt);
             vcur ^= 1;
+        }
+        if (overlap) {
+            cudaEventRecord(ev_chain, hs);
+            cudaStreamWaitEvent(c.s, ev_chain, 0);
         }
         ++sw;
     }
@@ -1340,7 +1375,7 @@ static int lg_alloc(const ModelDev &M, LgPtrs &L, void **owner) {
     const int nbk = ((d + 2 * BJ_B - 1) / (2 * BJ_B)) * 2, dp = nbk * BJ_B, bnp = nbk / 2;
     const size_t dpp = (size_t)dp * dp;
     const size_t obA = take(dpp), obT = take(dpp), obV0 = take(dpp), obV1 = take(dpp),
-                 obU = take((size_t)bnp * BJ_N * BJ_N), obL = take((size_t)bnp * BJ_N * BJ_N), obP = take(512),
+                 obU = take((size_t)2 * bnp * BJ_N * BJ_N), obL = take((size_t)bnp * BJ_N * BJ_N), obP = take(512),
                  obC = take((size_t)bnp);
     const size_t ndesc = (size_t)(nbk - 1) * 4 * bnp;
     const size_t obD = take((ndesc * sizeof(GemmArgs) + sizeof(double) - 1) / sizeof(double) + 2);
