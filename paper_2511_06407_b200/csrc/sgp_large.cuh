@@ -519,7 +519,10 @@ __global__ void k_lg_project(LgPtrs L, double tau, int field0, int field1, doubl
 #define BJ_B 32
 #define BJ_N (2 * BJ_B)
 #define BJ_INNER_CAP 60
-#define BJ_SMEM ((size_t)2 * BJ_N * (BJ_N + 1) * sizeof(double))
+// S and U (rows padded to BJ_N + 1), then the per-sweep rotation log: c and s of
+// every (step, pair) and the pivot indices (p = 0xff marks a skipped rotation)
+#define BJ_LOG_N ((BJ_N - 1) * (BJ_N / 2))
+#define BJ_SMEM ((size_t)2 * BJ_N * (BJ_N + 1) * sizeof(double) + (size_t)BJ_LOG_N * (2 * sizeof(double) + 2))
 
 __host__ __device__ inline void bj_pair(int r, int k, int nbk, int &I, int &J) {
     int a, b;
@@ -540,6 +543,8 @@ __global__ void __launch_bounds__(BJ_SOLVE_NT) k_bj_solve(const double *A, int d
     extern __shared__ double bjsm[];  // S and U, rows padded to BJ_N + 1
     double(*S)[BJ_N + 1] = reinterpret_cast<double(*)[BJ_N + 1]>(bjsm);
     double(*U)[BJ_N + 1] = reinterpret_cast<double(*)[BJ_N + 1]>(bjsm + BJ_N * (BJ_N + 1));
+    double *lc = bjsm + 2 * BJ_N * (BJ_N + 1), *ls = lc + BJ_LOG_N;
+    unsigned char *lp = reinterpret_cast<unsigned char *>(ls + BJ_LOG_N), *lq = lp + BJ_LOG_N;
     __shared__ double rc[BJ_N / 2], rs[BJ_N / 2], rt[BJ_N / 2], rpp[BJ_N / 2], rqq[BJ_N / 2];
     __shared__ int rp[BJ_N / 2], rq[BJ_N / 2], ract[BJ_N / 2];
     __shared__ int any, nrot;
@@ -583,6 +588,10 @@ __global__ void __launch_bounds__(BJ_SOLVE_NT) k_bj_solve(const double *A, int d
                 rp[tid] = p;
                 rq[tid] = q;
                 ract[tid] = act;
+                lc[rr * np + tid] = c;
+                ls[rr * np + tid] = sn;
+                lp[rr * np + tid] = act ? (unsigned char)p : (unsigned char)0xff;
+                lq[rr * np + tid] = (unsigned char)q;
                 const unsigned bal = __ballot_sync(0xffffffffu, act);
                 if (tid == 0 && bal) {
                     any = 1;
@@ -593,9 +602,9 @@ __global__ void __launch_bounds__(BJ_SOLVE_NT) k_bj_solve(const double *A, int d
             // fused two-sided update: thread (P, Q) owns the 2x2 block rows {p_P, q_P} x
             // cols {p_Q, q_Q}; row rotation P then column rotation Q, in registers
             // (the same rounded operations as a row pass followed by a column pass)
-            double nv[4], nu[2][2];
-            int bi[2], bj[2], ui[2];
-            bool act_blk = false, act_u[2] = {false, false};
+            double nv[4];
+            int bi[2], bj[2];
+            bool act_blk = false;
             if (tid < np * np) {
                 const int P = tid / np, Q = tid - P * np;
                 const bool aP = ract[P], aQ = ract[Q];
@@ -635,23 +644,6 @@ __global__ void __launch_bounds__(BJ_SOLVE_NT) k_bj_solve(const double *A, int d
                     }
                 }
             }
-            // columns p, q of U for two (row, pair) items per thread
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const int it = tid + h * blockDim.x;
-                if (it < np * m) {
-                    const int l = it / np, kk = it - l * np;
-                    ui[h] = it;
-                    if (ract[kk]) {
-                        act_u[h] = true;
-                        const int p = rp[kk], q = rq[kk];
-                        const double c = rc[kk], sn = rs[kk];
-                        const double up = U[l][p], uq = U[l][q];
-                        nu[h][0] = c * up - sn * uq;
-                        nu[h][1] = sn * up + c * uq;
-                    }
-                }
-            }
             __syncthreads();
             if (act_blk) {
                 S[bi[0]][bj[0]] = nv[0];
@@ -659,12 +651,33 @@ __global__ void __launch_bounds__(BJ_SOLVE_NT) k_bj_solve(const double *A, int d
                 S[bi[1]][bj[0]] = nv[2];
                 S[bi[1]][bj[1]] = nv[3];
             }
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                if (act_u[h]) {
-                    const int l = ui[h] / np, kk = ui[h] - l * np;
-                    U[l][rp[kk]] = nu[h][0];
-                    U[l][rq[kk]] = nu[h][1];
+            __syncthreads();
+        }
+        // U = U R_0 R_1 ... from the log, off the S chain: rows of U are independent,
+        // so one warp walks its rows through all steps with only warp-level syncs
+        // (each lane one pair of a step; the same rounded operations as a per-step update)
+        {
+            const int lane = tid & 31, nwarp = blockDim.x >> 5;
+            for (int l0 = tid >> 5; l0 < m; l0 += 2 * nwarp) {
+                const int l1 = l0 + nwarp;  // two rows per pass for latency overlap
+                const bool two = l1 < m;
+                for (int rr = 0; rr < m - 1; ++rr) {
+                    for (int kk = lane; kk < np; kk += 32) {
+                        const int p = lp[rr * np + kk];
+                        if (p != 0xff) {
+                            const int q = lq[rr * np + kk];
+                            const double c = lc[rr * np + kk], sn = ls[rr * np + kk];
+                            const double up0 = U[l0][p], uq0 = U[l0][q];
+                            const double up1 = two ? U[l1][p] : 0.0, uq1 = two ? U[l1][q] : 0.0;
+                            U[l0][p] = c * up0 - sn * uq0;
+                            U[l0][q] = sn * up0 + c * uq0;
+                            if (two) {
+                                U[l1][p] = c * up1 - sn * uq1;
+                                U[l1][q] = sn * up1 + c * uq1;
+                            }
+                        }
+                    }
+                    __syncwarp();
                 }
             }
             __syncthreads();
