@@ -125,3 +125,29 @@ def test_large_leapfrog_step_vs_oracle(large_case, order):
     assert rel_err(mt.eigenvalues, om.lam) < tol
     assert diag["fp_p_iters"] == odiag["fp_p_iters"]
     assert diag["fp_q_iters"] == odiag["fp_q_iters"]
+
+
+def test_block_jacobi_cold_decomposition(large_case):
+    """Chain-start cold decomposition on the large path (block Jacobi: pair solves on a
+    high-priority stream, eigenvector updates overlapped on the caller's stream) against
+    LAPACK: same spectrum, orthonormal basis, and Psi diag(lambda) Psi^T = sym(H) to the
+    reference's convergence tolerance (off-norm <= zeta ||H||_F, metric.py:101-109)."""
+    from paper_2511_06407_b200 import _native as nat
+
+    model, data, target, _ = large_case
+    d = target.dim
+    q = np.zeros((1, d))
+    h = target.device.eval(1.0, q, nat.EVAL_HESSIAN)["hess"][0]
+    hs = 0.5 * (h + h.T)
+    cfg = S.ChainConfig(epsilon=0.002, leapfrogs=1, moves=1, burnin=0, warm_order="parallel")
+    ch = S.DeviceChains(target.device, np.ones(1), cfg)
+    ch.set_q(q)
+    ch.init()
+    assert ch.status_host()[0] == 0
+    lam = ch.lam.cpu().numpy()[0]
+    psi = ch.psi.cpu().numpy()[0]
+    ref = np.linalg.eigvalsh(hs)
+    fro = np.linalg.norm(hs)
+    assert np.max(np.abs(np.sort(lam) - ref)) < 1e-11 * fro
+    assert np.max(np.abs(psi.T @ psi - np.eye(d))) < 1e-11
+    assert np.linalg.norm(psi @ np.diag(lam) @ psi.T - hs) < 1e-11 * fro
