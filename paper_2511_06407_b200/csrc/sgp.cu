@@ -247,7 +247,10 @@ extern "C" int sgp_model_destroy(sgp_model *m) {
     if (!m) return SGP_OK;
     cudaFree(m->d_phi);
     cudaFree(m->d_phis);
-    if (m->lg_owner) cudaFree(m->lg_owner);
+    if (m->lg_owner) {
+        lg_free_handles(m->lg);
+        cudaFree(m->lg_owner);
+    }
     cudaFree(m->d_y);
     cudaFree(m->d_cw);
     cudaFree(m->d_ckind);

@@ -30,7 +30,20 @@ struct LgPtrs {
     double *bjU, *bjLam, *bjPart;
     int *bjCnt;
     GemmArgs *bjDesc;            // [round][col A | row A | col V even | col V odd][2 * pairs]
+    // host handles owned by this workspace (one per model, like the buffers above): the
+    // high-priority stream of the block-Jacobi A chain and the events ordering it against
+    // the caller's stream (in, solved, chain, V update of even / odd rounds)
+    cudaStream_t bj_hs;
+    cudaEvent_t bj_ev[5];
 };
+
+static void lg_free_handles(LgPtrs &L) {
+    if (L.bj_hs) cudaStreamDestroy(L.bj_hs);
+    for (cudaEvent_t &e : L.bj_ev)
+        if (e) cudaEventDestroy(e);
+    L.bj_hs = nullptr;
+    for (cudaEvent_t &e : L.bj_ev) e = nullptr;
+}
 
 struct LargeWS {
     LgPtrs p;
@@ -1058,18 +1071,16 @@ static int lg_jacobi_block(LgCtx &c, int dst, double tol, double skip, int *swee
     // runs on a high-priority stream; the eigenvector update V' = V U, which nothing in the
     // chain reads, runs on the caller's stream and overlaps the next round's pair solve
     // (np CTAs, a fraction of the SMs).  U is double-buffered by round parity.
-    static cudaStream_t hs = nullptr;
-    static cudaEvent_t ev_in, ev_solved, ev_chain, ev_v[2];
-    static bool overlap = true;
-    if (!hs) {
-        int lo = 0, hi = 0;
-        cudaDeviceGetStreamPriorityRange(&lo, &hi);
-        cudaStreamCreateWithPriority(&hs, cudaStreamNonBlocking, hi);
-        for (cudaEvent_t *e : {&ev_in, &ev_solved, &ev_chain, &ev_v[0], &ev_v[1]})
-            cudaEventCreateWithFlags(e, cudaEventDisableTiming);
+    static bool overlap_env = true, overlap_read = false;
+    if (!overlap_read) {
         const char *e = getenv("SGP_BJ_OVERLAP");  // 0: everything on the caller's stream (A/B timing)
-        overlap = !(e && e[0] == '0');
+        overlap_env = !(e && e[0] == '0');
+        overlap_read = true;
     }
+    const bool overlap = overlap_env && c.L.bj_hs;
+    cudaStream_t hs = c.L.bj_hs;
+    const cudaEvent_t ev_in = c.L.bj_ev[0], ev_solved = c.L.bj_ev[1], ev_chain = c.L.bj_ev[2];
+    const cudaEvent_t ev_v[2] = {c.L.bj_ev[3], c.L.bj_ev[4]};
     cudaStream_t as = overlap ? hs : c.s;
     int vcur = 0, sw = 0;
     const size_t per_round = (size_t)4 * np;
@@ -1424,9 +1435,19 @@ static int lg_alloc(const ModelDev &M, LgPtrs &L, void **owner) {
     L.bjCnt = reinterpret_cast<int *>(base + obC);
     L.bjDesc = reinterpret_cast<GemmArgs *>(base + ((obD + 1) & ~size_t(1)));  // 16-byte aligned
     {
+        L.bj_hs = nullptr;
+        for (cudaEvent_t &e : L.bj_ev) e = nullptr;
+        int lo = 0, hi = 0;
+        bool ok = cudaDeviceGetStreamPriorityRange(&lo, &hi) == cudaSuccess &&
+                  cudaStreamCreateWithPriority(&L.bj_hs, cudaStreamNonBlocking, hi) == cudaSuccess;
+        for (cudaEvent_t &e : L.bj_ev) ok = ok && cudaEventCreateWithFlags(&e, cudaEventDisableTiming) == cudaSuccess;
+        if (!ok) lg_free_handles(L);  // no overlap: the block Jacobi then runs on the caller's stream
+    }
+    {
         std::vector<GemmArgs> desc;
         bj_build_desc(L, desc);
         if (cudaMemcpy(L.bjDesc, desc.data(), desc.size() * sizeof(GemmArgs), cudaMemcpyHostToDevice) != cudaSuccess) {
+            lg_free_handles(L);
             cudaFree(base);
             return SGP_ENOMEM;
         }
