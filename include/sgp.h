@@ -131,7 +131,9 @@ typedef struct sgp_chain_config {
     int gs_interval;
     int sweep_cap;
     int metric;         /* SGP_METRIC_* */
-    int warm_order;     /* SGP_ORDER_* */
+    int warm_order;     /* SGP_ORDER_* of warm decompositions (dynamic_eigendecompose) */
+    int cold_order;     /* SGP_ORDER_* of cold decompositions (static_eigendecompose); the
+                           fused small-d kernel always uses the reference order */
 } sgp_chain_config;
 
 /* Per-move records (ChainRecord, sampler.py:86-99), arrays of moves*Z

@@ -88,7 +88,7 @@ class ChainConfigC(ctypes.Structure):
     _fields_ = [("epsilon", ctypes.c_double), ("leapfrogs", ctypes.c_int), ("kappa", ctypes.c_double),
                 ("zeta", ctypes.c_double), ("fp_max_iters", ctypes.c_int), ("fp_tol", ctypes.c_double),
                 ("gs_interval", ctypes.c_int), ("sweep_cap", ctypes.c_int), ("metric", ctypes.c_int),
-                ("warm_order", ctypes.c_int)]
+                ("warm_order", ctypes.c_int), ("cold_order", ctypes.c_int)]
 
 
 class GridSpecC(ctypes.Structure):

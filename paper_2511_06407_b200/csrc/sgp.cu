@@ -464,9 +464,78 @@ __global__ void __launch_bounds__(SGP_MAX_NT) k_eigh_cold(int d, const double *H
     if (threadIdx.x == 0) sweeps[z] = sw;
 }
 
+// d at and above which cold decompositions use the grid-wide reference-order Jacobi
+// (sgp_jbig.cuh) instead of one CTA per matrix; SGP_JBIG_MIN_D overrides (tests)
+static int jbig_min_d() {
+    const char *e = getenv("SGP_JBIG_MIN_D");
+    return e ? atoi(e) : 257;
+}
+
+__global__ void k_sym_eye(const double *H, double *A, double *V, int d) {
+    for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < (size_t)d * d;
+         idx += (size_t)gridDim.x * blockDim.x) {
+        const int i = (int)(idx / d), k = (int)(idx - (size_t)i * d);
+        A[idx] = (i == k) ? H[idx] : 0.5 * (H[idx] + H[(size_t)k * d + i]);
+        V[idx] = (i == k) ? 1.0 : 0.0;
+    }
+}
+__global__ void k_frob_part(const double *A, size_t n, double *part) {
+    __shared__ double red[32];
+    double acc = 0.0;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+        acc += A[i] * A[i];
+    acc = warp_sum(acc);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+        part[blockIdx.x] = t;
+    }
+}
+__global__ void k_copy_diag(const double *A, int d, double *lam) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < d; i += gridDim.x * blockDim.x) lam[i] = A[(size_t)i * d + i];
+}
+
+// Cold decomposition of one large matrix through sgp_jbig.cuh (metric.py:112-127)
+static int eigh_cold_big(int Z, int d, const double *d_h, double zeta, int cap, double *d_lam, double *d_psi,
+                         int *d_sweeps, cudaStream_t s) {
+    const size_t dd = (size_t)d * d;
+    double *A = nullptr, *part = nullptr;
+    CUDA_TRY(cudaMalloc(&A, sizeof(double) * dd));
+    CUDA_TRY(cudaMalloc(&part, sizeof(double) * 148));
+    JbWS w;
+    int rc = SGP_OK;
+    std::vector<int> sw(Z);
+    for (int z = 0; z < Z && rc == SGP_OK; ++z) {
+        k_sym_eye<<<148 * 4, 256, 0, s>>>(d_h + z * dd, A, d_psi + z * dd, d);
+        k_frob_part<<<148, 256, 0, s>>>(A, dd, part);
+        std::vector<double> hp(148);
+        cudaMemcpyAsync(hp.data(), part, sizeof(double) * 148, cudaMemcpyDeviceToHost, s);
+        if (cudaStreamSynchronize(s) != cudaSuccess) {
+            rc = SGP_ECUDA;
+            break;
+        }
+        double t = 0.0;
+        for (double v : hp) t += v;
+        const double tol = zeta * sqrt(t), skip = tol / d;
+        const int r = jb_jacobi(w, A, d_psi + z * dd, d, tol, skip, cap, s);
+        if (r == -2) rc = SGP_ECUDA;
+        sw[z] = r < 0 ? -1 : r;
+        k_copy_diag<<<8, 256, 0, s>>>(A, d, d_lam + (size_t)z * d);
+    }
+    if (rc == SGP_OK) cudaMemcpyAsync(d_sweeps, sw.data(), sizeof(int) * Z, cudaMemcpyHostToDevice, s);
+    cudaStreamSynchronize(s);
+    jb_ws_free(w);
+    cudaFree(A);
+    cudaFree(part);
+    return rc;
+}
+
 extern "C" int sgp_eigh_cold(int Z, int d, const double *d_h, double zeta, int cap, double *d_lam, double *d_psi,
                              int *d_sweeps, void *stream) {
     if (Z < 1 || d < 1 || !d_h || !d_lam || !d_psi || !d_sweeps) return SGP_EINVAL;
+    if (d >= jbig_min_d() && d >= 2) return eigh_cold_big(Z, d, d_h, zeta, cap, d_lam, d_psi, d_sweeps, S(stream));
     double *tmp = nullptr;
     CUDA_TRY(cudaMallocAsync(&tmp, sizeof(double) * Z * ((size_t)d * d + sgp_jacobi_log_doubles(d)), S(stream)));
     k_eigh_cold<<<Z, SGP_MAX_NT, 0, S(stream)>>>(d, d_h, zeta, cap, d_lam, d_psi, d_sweeps, tmp);

@@ -6,10 +6,10 @@
 //   trace     Y_j1 = Phi_j1 W[blk j1, :], s^(j1 j2)_i = <Y_j1[i, blk j2], phi_j2(x_i)>   (:495-509)
 //   metric    W = Psi M Psi^T, M = diag((lam/g)/g) - (b b^T) o T       (metric.py:188-204)
 //   warm eigh A = Psi^T H Psi                                           (metric.py:170)
-// The warm Jacobi uses the round-robin parallel order grid-wide (d/2
-// rotations per round, rows then columns), with the reference's skip rule
-// and convergence test; cold decompositions keep the reference order
-// (bit-exact, one warp; only at chain start and rejections).  The O(d) and
+// Warm decompositions use the block Jacobi (round-robin order of 64 x 64 pair
+// problems, warm_order="parallel") or the reference's cyclic order (sgp_jbig.cuh,
+// bit-exact); cold decompositions keep the reference order unless
+// cold_order="parallel" (chain start, rejections, rung starts).  The O(d) and
 // O(N d) glue (per-sample derivatives, prior terms, mat-vecs, fixed-point
 // updates) reuses the CTA-level functions on one CTA.  The leapfrog control
 // flow runs on the host thread, reading back one status/delta word per
@@ -17,6 +17,7 @@
 #pragma once
 #include "sgp_chain.cuh"
 #include "sgp_gemm.cuh"
+#include "sgp_jbig.cuh"
 
 #define LG_NT 256
 
@@ -35,9 +36,16 @@ struct LgPtrs {
     // the caller's stream (in, solved, chain, V update of even / odd rounds)
     cudaStream_t bj_hs;
     cudaEvent_t bj_ev[5];
+    // reference-order Jacobi (sgp_jbig.cuh) workspace, allocated on first use
+    JbWS *jb;
 };
 
 static void lg_free_handles(LgPtrs &L) {
+    if (L.jb) {
+        jb_ws_free(*L.jb);
+        delete L.jb;
+        L.jb = nullptr;
+    }
     if (L.bj_hs) cudaStreamDestroy(L.bj_hs);
     for (cudaEvent_t &e : L.bj_ev)
         if (e) cudaEventDestroy(e);
@@ -1131,11 +1139,12 @@ static int lg_jacobi_block(LgCtx &c, int dst, double tol, double skip, int *swee
 static int lg_jacobi(LgCtx &c, int dst, double tol, double skip, bool parallel, int *sweeps) {
     const int d = c.d;
     if (!parallel) {
-        k_lg_set2<<<1, 1, 0, c.s>>>(c.L.sc + 9, tol, skip);
-        lg_op(c, LG_JCYC, dst);
-        lg_sync(c);
-        *sweeps = c.si[4];
-        return c.status;
+        // reference pivot order, bit-identical (sgp_jbig.cuh); H is symmetric here
+        if (!c.L.jb) return SGP_STATUS_JACOBI;
+        const int sw = jb_jacobi(*c.L.jb, c.L.H, c.L.P[dst], d, tol, skip, c.cfg.sweep_cap, c.s);
+        if (sw == -2) return SGP_STATUS_JACOBI;
+        *sweeps = sw;
+        return sw < 0 ? SGP_STATUS_JACOBI : 0;
     }
     const char *sj = getenv("SGP_LG_SCALAR_JACOBI");
     if (!(sj && sj[0] == '1') && c.L.bjA) return lg_jacobi_block(c, dst, tol, skip, sweeps);
@@ -1166,7 +1175,9 @@ static int lg_eig_cold(LgCtx &c, int dst, int *sweeps) {
     const double hnorm = lg_hnorm(c);
     const double tol = c.cfg.zeta * hnorm, skip = d ? tol / d : 0.0;
     k_lg_eye<<<lg_blocks((size_t)d * d), 256, 0, c.s>>>(c.L.P[dst], d);
-    const int st = lg_jacobi(c, dst, tol, skip, c.cfg.warm_order == SGP_ORDER_PARALLEL, sweeps);
+    // cold decompositions keep the reference's pivot order unless cold_order says otherwise
+    // (the momentum p = Psi (sqrt(g) o z) depends on Psi's column order: SURVEY.md M6)
+    const int st = lg_jacobi(c, dst, tol, skip, c.cfg.cold_order == SGP_ORDER_PARALLEL, sweeps);
     if (st) return st;
     lg_op(c, LG_GLAM, dst, 0, 0, 0);
     c.since[dst] = 0;
@@ -1452,6 +1463,7 @@ static int lg_alloc(const ModelDev &M, LgPtrs &L, void **owner) {
             return SGP_ENOMEM;
         }
     }
+    L.jb = new JbWS();
     *owner = base;
     return SGP_OK;
 }

@@ -55,6 +55,7 @@ class ChainConfig:
     seed: object = 0
     record_q: bool = False
     warm_order: str = "cyclic"
+    cold_order: str = "cyclic"
 
     def __post_init__(self):
         if self.epsilon <= 0.0:
@@ -77,6 +78,8 @@ class ChainConfig:
             raise ValueError(f"metric must be one of {METRIC_MODES}")
         if self.warm_order not in WARM_ORDERS:
             raise ValueError(f"warm_order must be one of {WARM_ORDERS}")
+        if self.cold_order not in WARM_ORDERS:
+            raise ValueError(f"cold_order must be one of {WARM_ORDERS}")
 
     def to_c(self):
         c = nat.ChainConfigC()
@@ -85,6 +88,7 @@ class ChainConfig:
         c.gs_interval, c.sweep_cap = int(self.gs_interval or 0), self.sweep_cap
         c.metric = nat.METRIC_CODES[self.metric]
         c.warm_order = nat.ORDER_CODES[self.warm_order]
+        c.cold_order = nat.ORDER_CODES[self.cold_order]
         return c
 
 
