@@ -19,13 +19,34 @@ from .metric import (  # noqa: F401
     static_eigendecompose, t_matrix, w1_matrix, w2_matrix,
 )
 from .posterior import (  # noqa: F401
-    DivergenceError, DomainError, ParamVector, PosteriorTarget, gradient, hessian,
-    neg_log_posterior, potential_derivatives, trace_contractions,
+    DivergenceError, DomainError, ParamVector, PosteriorTarget, QuadraticTarget, dense_oracle, gradient,
+    hessian, neg_log_posterior, potential_derivatives, trace_contractions,
 )
 from .sampler import (  # noqa: F401
     ChainConfig, ChainError, ChainRecord, ChainResult, euclidean_hmc_run, grad_q_hamiltonian,
     hamiltonian, leapfrog_step, rank_sum_test, read_jsonl, rmhmc_run, run_chain, run_chains,
     wilcoxon_split_half, write_jsonl,
 )
+from .evidence import (  # noqa: F401
+    EvidenceEstimate, GridSpec, TemperLadder, default_ladder, laplace_full, laplace_grid_oracle,
+    thermo_integrate, ti_variance,
+)
+
+# the reference's public names (softabs_gp/__init__.py:75-132), plus this package's extras
+__all__ = [
+    "BetancourtCache", "ChainConfig", "ChainError", "ChainRecord", "ChainResult", "Dataset",
+    "DivergenceError", "DomainError", "EvidenceEstimate", "GridSpec", "JacobiError", "KernelSpec",
+    "MetricState", "ModelSpec", "ParamVector", "PosteriorTarget", "SchemaError", "TemperLadder",
+    "TruthRecord", "build_cache", "build_model", "default_ladder", "dense_oracle",
+    "dynamic_eigendecompose", "euclidean_hmc_run", "feature_value", "grad_q_hamiltonian", "gradient",
+    "hamiltonian", "hessian", "laplace_full", "laplace_grid_oracle", "leapfrog_step", "metric_apply",
+    "metric_apply_inverse", "metric_from_hessian", "neg_log_posterior", "potential_derivatives",
+    "rank_sum_test", "read_csv", "read_jsonl", "rmhmc_run", "run_chain", "sample_momentum",
+    "simulate_logistic", "simulate_meanvar", "softabs", "softabs_deriv", "spectral_variance",
+    "static_eigendecompose", "t_matrix", "thermo_integrate", "ti_variance", "trace_contractions",
+    "write_csv", "write_jsonl",
+    # extras
+    "QuadraticTarget", "run_chains",
+]
 
 __version__ = "0.1.0"

@@ -27,7 +27,7 @@ import numpy as np
 
 from .metric import JacobiError
 from .posterior import PosteriorTarget
-from .sampler import ChainConfig, ChainError, run_chain, run_chains, wilcoxon_split_half
+from .sampler import ChainConfig, ChainError, as_chain_config, run_chain, run_chains, wilcoxon_split_half
 
 
 @dataclasses.dataclass(frozen=True)
@@ -185,34 +185,60 @@ def _dist_info():
     return None, 0, 1
 
 
-def gather_chain_values(local_ids, local_values, n_chains, n_rungs):
-    """All-gather per-chain rung values to every rank; returns (Z, S) in chain order.
+# The ChainError texts a device chain can end with (sampler.py:349,389 wording); they travel
+# through the all-gather as small integer codes so the warnings keep the reference's text.
+CHAIN_ERROR_TEXTS = (
+    None,
+    "divergence on the first move; initial point or epsilon unusable",
+    "chain start failed: non-finite or invalid initial state",
+    "chain failed",
+)
 
-    One ``all_gather_into_tensor`` of a padded [ceil(Z/W), S+1] block per rank
-    (column 0 = chain id + 1, 0 marks padding).  NCCL for GPU ranks, gloo on CPU.
+
+def _error_code(err):
+    if err is None:
+        return 0
+    try:
+        return CHAIN_ERROR_TEXTS.index(err)
+    except ValueError:
+        return len(CHAIN_ERROR_TEXTS) - 1
+
+
+def gather_chain_values(local_ids, local_values, n_chains, n_rungs, local_errors=None, return_errors=False):
+    """All-gather per-chain rung values to every rank; returns (Z, S) in chain order
+    (and, with ``return_errors``, each chain's error text or None).
+
+    One ``all_gather_into_tensor`` of a padded [ceil(Z/W), S+2] block per rank (column 0 =
+    chain id + 1, 0 marks padding; column 1 = error code).  NCCL for GPU ranks, gloo on CPU.
     """
     import torch
 
     dist, rank, world = _dist_info()
     full = np.full((n_chains, n_rungs), np.nan)
+    errors = [None] * n_chains
+    local_errors = local_errors or [None] * len(local_ids)
     if dist is None or world == 1:
         for k, z in enumerate(local_ids):
             full[z] = local_values[k]
-        return full
+            errors[z] = local_errors[k]
+        return (full, errors) if return_errors else full
     per = (n_chains + world - 1) // world
-    block = np.zeros((per, n_rungs + 1))
+    block = np.zeros((per, n_rungs + 2))
     for k, z in enumerate(local_ids):
         block[k, 0] = z + 1
-        block[k, 1:] = local_values[k]
+        block[k, 1] = _error_code(local_errors[k])
+        block[k, 2:] = local_values[k]
     dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
     src = torch.as_tensor(block, dtype=torch.float64, device=dev)
-    out = torch.empty((world * per, n_rungs + 1), dtype=torch.float64, device=dev)
+    out = torch.empty((world * per, n_rungs + 2), dtype=torch.float64, device=dev)
     dist.all_gather_into_tensor(out, src)
     allb = out.cpu().numpy()
     for row in allb:
         if row[0] > 0:
-            full[int(row[0]) - 1] = row[1:]
-    return full
+            z = int(row[0]) - 1
+            full[z] = row[2:]
+            errors[z] = CHAIN_ERROR_TEXTS[int(row[1])]
+    return (full, errors) if return_errors else full
 
 
 def thermo_integrate(model, data, ladder, config, *, rung_average=False, warmup_segment_moves=50,
@@ -226,8 +252,10 @@ def thermo_integrate(model, data, ladder, config, *, rung_average=False, warmup_
     ``warmup_runner`` substitute the chain executors (tests inject the CPU
     oracle to exercise the multi-rank logic without a GPU).
     """
-    if not isinstance(config, ChainConfig) and ladder_runner is None:
-        raise TypeError("config must be a ChainConfig")
+    if ladder_runner is None:
+        if not hasattr(config, "epsilon") or not hasattr(config, "leapfrogs"):
+            raise TypeError("config must be a ChainConfig")
+        config = as_chain_config(config)
     seed_root = config.seed if isinstance(config.seed, np.random.SeedSequence) \
         else np.random.SeedSequence(config.seed)
     n_chains = ladder.chains
@@ -242,15 +270,17 @@ def thermo_integrate(model, data, ladder, config, *, rung_average=False, warmup_
     runner = ladder_runner or device_ladder_runner
     vals, errs = runner(target, [seqs[warmup_max_segments + z] for z in mine], q_warm, ladder, config,
                         rung_average, spread_moves)
-    # failure flags travel as an all-NaN row (the reference maps them to NaN too)
-    rung_values = gather_chain_values(mine, vals, n_chains, ladder.size)
+    # failed chains travel as an all-NaN row plus their error code (the reference maps them
+    # to NaN and keeps the ChainError text in the warning, evidence.py:248-253)
+    rung_values, chain_errors = gather_chain_values(mine, vals, n_chains, ladder.size, errs,
+                                                    return_errors=True)
     if progress is not None:
         progress(f"evidence: {n_chains} chains finished on {world} rank(s)")
     per_chain = []
     for z in range(n_chains):
         row = rung_values[z]
-        if np.all(np.isnan(row)):
-            warnings.append(f"chain {z} flagged: chain failed")
+        if chain_errors[z] is not None or np.all(np.isnan(row)):
+            warnings.append(f"chain {z} flagged: {chain_errors[z] or 'chain failed'}")
             per_chain.append(math.nan)
             continue
         per_chain.append(trapezoid(row, ladder.taus))

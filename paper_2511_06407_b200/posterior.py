@@ -9,7 +9,9 @@ assembled once per (model, data) in HBM and shared across temperatures
 
 from __future__ import annotations
 
+import collections
 import ctypes
+import hashlib
 import math
 from dataclasses import dataclass
 
@@ -194,6 +196,37 @@ class FeatureCacheView:
         return self._phi
 
 
+# Device models are shared by every target built on the same (model, data): the design
+# matrices are assembled once in HBM (posterior.py:261-264 shares the FeatureCache across
+# temperatures the same way), so callers that rebuild a PosteriorTarget per rung or per call
+# -- the reference's evidence loop through the drop-in shim -- do not re-upload Phi.
+_DEVICE_CACHE: "collections.OrderedDict[tuple, DeviceModel]" = collections.OrderedDict()
+_DEVICE_CACHE_MAX = 8
+
+
+def _fingerprint(model, data):
+    h = hashlib.sha1()
+    for a in (data.x, data.y):
+        a = np.ascontiguousarray(np.asarray(a, dtype=float))
+        h.update(str(a.shape).encode())
+        h.update(a.tobytes())
+    return (repr(model), h.hexdigest())
+
+
+def shared_device(model, data):
+    """The DeviceModel of (model, data), created on first use and cached (LRU)."""
+    key = _fingerprint(model, data)
+    dev = _DEVICE_CACHE.get(key)
+    if dev is not None:
+        _DEVICE_CACHE.move_to_end(key)
+        return dev
+    dev = DeviceModel(model, data)
+    _DEVICE_CACHE[key] = dev
+    while len(_DEVICE_CACHE) > _DEVICE_CACHE_MAX:
+        _DEVICE_CACHE.popitem(last=False)
+    return dev
+
+
 class PosteriorTarget:
     """Callable bundle for one (model, data, temperature) triple (posterior.py:195-307)."""
 
@@ -207,7 +240,7 @@ class PosteriorTarget:
             self.layout, self.device = _shared
         else:
             self.layout = BlockLayout.from_model(model)
-            self.device = DeviceModel(model, data)
+            self.device = shared_device(model, data)
             if self.device.dim != self.layout.dim:
                 raise RuntimeError("device layout disagrees with BlockLayout")
         self.cache = FeatureCacheView(self.device, len(model.functions))
@@ -353,3 +386,104 @@ def potential_derivatives(likelihood, f, y, *, variance_floor=1e-3):
     if single:
         return tuple(a[0] for a in out)
     return out
+
+
+# -- constant-Hessian Gaussian target (reference tests/conftest.py:14-61) -------
+
+
+class QuadraticState:
+    """State of a QuadraticTarget, evaluated on the device (SGP_LIK_QUADRATIC):
+    U = 0.5 (q-m)^T P (q-m) - tau c, gradient P (q-m), Hessian P, dH/dq = 0."""
+
+    def __init__(self, target, q):
+        self.target = target
+        self.q = np.ascontiguousarray(np.asarray(q, dtype=float))
+        if self.q.shape != (target.dim,):
+            raise ValueError(f"expected point of dimension {target.dim}, got {self.q.shape}")
+        self._out = None
+
+    def _eval(self):
+        if self._out is None:
+            out = self.target.device.eval(self.target.tau, self.q[None, :],
+                                          nat.EVAL_POTENTIAL | nat.EVAL_GRADIENT | nat.EVAL_HESSIAN)
+            raise_status(int(out["status"][0]), "quadratic target")
+            self._out = out
+        return self._out
+
+    def potential(self):
+        return float(self._eval()["pot"][0])
+
+    def gradient(self):
+        return self._eval()["grad"][0]
+
+    def hessian(self):
+        return self._eval()["hess"][0]
+
+    def sum_potentials(self):
+        return -self.target.loglik_const
+
+    def trace_single(self, w):
+        t, status = self.target.device.trace(self.target.tau, self.q[None, :], np.asarray(w, dtype=float)[None])
+        raise_status(int(status[0]), "trace_single")
+        return t[0]
+
+
+class QuadraticTarget:
+    """Gaussian 'posterior' with constant Hessian, injectable into the sampler and the
+    evidence machinery exactly like the reference's test fake (tests/conftest.py:36-61),
+    but evaluated by libsgp so the device sampler can run it (no CPU fallback)."""
+
+    def __init__(self, precision, mean=None, loglik_const=0.0, tau=1.0, *, _device=None):
+        self.precision = np.ascontiguousarray(np.asarray(precision, dtype=float))
+        self.dim = self.precision.shape[0]
+        self.mean = np.zeros(self.dim) if mean is None else np.asarray(mean, dtype=float)
+        self.loglik_const = float(loglik_const)
+        self.tau = float(tau)
+        self.device = _device if _device is not None else DeviceModel(
+            None, None, quadratic=(self.precision, self.mean, self.loglik_const))
+
+    def initial_point(self):
+        return np.zeros(self.dim)
+
+    def at(self, q):
+        return QuadraticState(self, q)
+
+    def at_temperature(self, tau):
+        return QuadraticTarget(self.precision, self.mean, self.loglik_const, tau, _device=self.device)
+
+    def log_likelihood(self, q):
+        return self.loglik_const
+
+    def log_likelihoods(self, qs):
+        return np.full(np.atleast_2d(qs).shape[0], self.loglik_const)
+
+
+# -- dense finite-difference trace oracle (posterior.py:582-615) ---------------
+
+
+def dense_oracle(w, q, model: ModelSpec, data: Dataset, *, tau=None, target=None, step: float = 1e-5,
+                 dim_cap: int = 200):
+    """Trace contraction t_i = sum(W o dH/dq_i) from central differences of the Hessian,
+    the reference's self-check of trace_single.  The 2d perturbed Hessians are evaluated
+    in one batched device call instead of 2d sequential ones."""
+    q, tau = _split_param(q, tau)
+    target = _resolve(target, model, data, tau)
+    d = target.dim
+    if d > dim_cap:
+        raise ValueError(f"dense_oracle guarded to d <= {dim_cap}, got d = {d}")
+    w = np.asarray(w, dtype=float)
+    w = 0.5 * (w + w.T)
+    hs = np.array([step * max(1.0, abs(q[i])) for i in range(d)])
+    pts = np.repeat(q[None, :], 2 * d, axis=0)
+    idx = np.arange(d)
+    pts[2 * idx, idx] += hs
+    pts[2 * idx + 1, idx] -= hs
+    out = target.device.eval(target.tau, pts, nat.EVAL_HESSIAN)
+    for code in out["status"]:
+        raise_status(int(code), "dense_oracle")
+    hess = out["hess"]
+    t = np.empty(d)
+    for i in range(d):
+        dh = (hess[2 * i] - hess[2 * i + 1]) / (2.0 * hs[i])
+        t[i] = float(np.sum(w * dh))
+    return t

@@ -92,6 +92,35 @@ class ChainConfig:
         return c
 
 
+def as_chain_config(config) -> ChainConfig:
+    """This package's ChainConfig from any object carrying the reference's ChainConfig
+    fields by name (sampler.py:53-65), e.g. ``softabs_gp.sampler.ChainConfig`` handed over by
+    reference code through the drop-in shim.  Fields the object lacks keep their defaults, so
+    a reference config runs with ``warm_order = cold_order = "cyclic"`` (the reference's
+    order)."""
+    if isinstance(config, ChainConfig):
+        return config
+    kw = {f.name: getattr(config, f.name) for f in dataclasses.fields(ChainConfig) if hasattr(config, f.name)}
+    return ChainConfig(**kw)
+
+
+def as_device_target(target):
+    """A libsgp-backed target for ``target``: returned as is when it already is one;
+    a reference ``PosteriorTarget`` (model, data, tau) or the reference's constant-Hessian
+    test fake (precision, mean, loglik_const, tau) is rebuilt on the shared device model."""
+    if hasattr(target, "device"):
+        return target
+    if hasattr(target, "model") and hasattr(target, "data"):
+        return PosteriorTarget(target.model, target.data, float(getattr(target, "tau", 1.0)))
+    if hasattr(target, "precision"):
+        from .posterior import QuadraticTarget
+
+        return QuadraticTarget(target.precision, getattr(target, "mean", None),
+                               getattr(target, "loglik_const", 0.0), float(getattr(target, "tau", 1.0)))
+    raise TypeError(f"cannot run {type(target).__name__} on the device: it is neither a "
+                    "PosteriorTarget nor a constant-Hessian target")
+
+
 @dataclasses.dataclass
 class ChainRecord:
     move: int
@@ -289,6 +318,8 @@ def run_chains(target, config: ChainConfig, seeds, initials=None, taus=None):
     """
     import torch
 
+    target = as_device_target(target)
+    config = as_chain_config(config)
     Z = len(seeds)
     d = target.dim
     taus = np.full(Z, target.tau) if taus is None else np.asarray(taus, dtype=float)
@@ -334,6 +365,8 @@ def run_chains(target, config: ChainConfig, seeds, initials=None, taus=None):
 
 def run_chain(target, config, *, initial=None):
     """One MCMC chain (sampler.py:331-418), move loop on the device."""
+    target = as_device_target(target)
+    config = as_chain_config(config)
     q0 = np.asarray(target.initial_point() if initial is None else initial, dtype=float).copy()
     if q0.shape != (target.dim,):
         raise ValueError("initial point has wrong dimension")
@@ -384,6 +417,8 @@ def leapfrog_step(q, p, metric, target, config):
     """One generalized leapfrog from (q, p) (sampler.py:280-292), on the device."""
     import torch
 
+    target = as_device_target(target)
+    config = as_chain_config(config)
     q = np.asarray(q, dtype=float)
     p = np.asarray(p, dtype=float)
     d = target.dim
