@@ -1,21 +1,24 @@
 """Benchmark: generalized-leapfrog steps/sec of the SoftAbs RMHMC inner loop.
 
-Workload (BASELINE.json configs[1]): single-kernel GP
-binary classification, simulate_logistic(1, n=512, seed=0), logistic model
-with 30 basis functions (d = 34), epsilon = 1e-3, C = 100 leapfrogs per move,
-reference warm-Jacobi order (trajectory parity with the reference).  Z
-independent chains per GPU ("replicas", one CTA each).  One step = one MH
-move (C generalized leapfrogs + Metropolis test) of every chain on the GPU.
+Default workload (the largest single-GPU config of BASELINE.json, configs[3]; SURVEY.md 8(d)
+C4): the multiple-kernel mean/variance GP model scaled to N = 8192 rows,
+simulate_meanvar(34, 19, n=8192, seed=0) with the "nl-meanvar" preset (d = 2083), epsilon =
+1e-4, C = 100 leapfrogs per move, one chain per GPU ("replicas": a chain is never split
+across GPUs).  One step = one MH move (C generalized leapfrogs + the Metropolis test).  Warm
+decompositions use the block Jacobi (warm_order="parallel"); cold ones (chain start,
+rejections) the reference's pivot order, bit-identical (sgp_jbig.cuh).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--chains Z]
-    python bench.py --impl reference     # the reference algorithm on host cores
+    python bench.py [--gpus N] [--steps K] [--warmup W]            # C4 (headline)
+    python bench.py --workload c2                                  # C2: 1776 chains, d = 34
+    python bench.py --impl reference [--workload c4|c2]            # reference algorithm, host cores
 
-``value`` = chain-leapfrogs/s over all ranks (device time, max over ranks);
-``e2e`` = the same through the public chain API with host RNG, pinned H2D of
-the step's normals/uniforms and D2H of the move records inside the timed
-region.  The CPU arms run the oracle port (oracle/, the reference algorithm
-restated: numpy BLAS + the C Jacobi) because the reference package cannot
-travel to the GPU box.
+``value`` = chain-leapfrogs/s over all ranks (CUDA events on the launching stream, max over
+ranks); ``e2e`` = the same through the public chain API with host RNG draws, pinned H2D of the
+step's normals/uniforms and D2H of the move records and positions inside the timed region.
+The CPU arms run the oracle port (oracle/: the reference algorithm restated, numpy/OpenBLAS
++ the C restatement of the Numba Jacobi) because the reference package cannot travel to the
+GPU box; at C4 a leapfrog takes minutes on the host, so the CPU figure is a bounded sample of
+its parts scaled by the canonical per-leapfrog call counts (cpu_c4_sample).
 """
 
 from __future__ import annotations
@@ -38,12 +41,20 @@ sys.path.insert(0, ROOT)
 METRIC = "generalized-leapfrog steps/sec"
 UNIT = "chain-leapfrogs/s"
 EPS, LEAPFROGS, N_ROWS = 1e-3, 100, 512
+C4_EPS, C4_LEAPFROGS = 1e-4, 100
+C4_NAME = ("C4 multiple-kernel mean/variance GP (nl-meanvar), N=8192 rows, 34 continuous + 19 binary "
+           "covariates, d=2083, eps=1e-4, C=100")
+C2_NAME = "C2 logistic GP classification N=512 d=34, eps=1e-3, C=100"
 
 
-def canonical_flops_per_leapfrog(N, D, d, fp_p=3, fp_q=3, s=5.0 / 3.0):
-    """SURVEY.md 8(d) canonical FLOP count of one generalized leapfrog (J = 1)."""
+def canonical_flops_per_leapfrog(N, Ds, d, fp_p=3, fp_q=3, s=5.0 / 3.0):
+    """SURVEY.md 8(d) canonical FLOP count of one generalized leapfrog; Ds = (D_1, ..., D_J)."""
+    if not isinstance(Ds, (list, tuple)):
+        Ds = (Ds,)
     n_tr = fp_p + 2
-    return n_tr * (2 * N * D * D + 4 * d ** 3) + 2 * d ** 3 + fp_q * (2 * N * D * D + (6.2 + 6 * s) * d ** 3)
+    dsum = sum(Ds)
+    pairs = sum(Ds[a] * Ds[b] for a in range(len(Ds)) for b in range(a, len(Ds)))
+    return n_tr * (2 * N * dsum * dsum + 4 * d ** 3) + 2 * d ** 3 + fp_q * (2 * N * pairs + (6.2 + 6 * s) * d ** 3)
 
 
 def workload():
@@ -52,6 +63,62 @@ def workload():
     data, _ = rrgp.simulate_logistic(1, n=N_ROWS, seed=0)
     model = rrgp.build_model("logistic", data.x)
     return model, data
+
+
+def workload_c4():
+    from paper_2511_06407_b200 import rrgp
+
+    data, _ = rrgp.simulate_meanvar(34, 19, n=8192, seed=0)
+    model = rrgp.build_model("nl-meanvar", data.x)
+    return model, data
+
+
+def c4_feature_widths(model):
+    return tuple(sum(k.features for k in ks) + 1 for ks in model.functions)
+
+
+def cpu_c4_sample(reps=1):
+    """The reference algorithm's C4 leapfrog on this host, as a bounded sample: one Hessian
+    (posterior.py:442-482), one structured trace (posterior.py:486-542) and one d^3 GEMM in
+    numpy/OpenBLAS with every host thread, plus a slice of a cyclic Jacobi sweep in the C
+    restatement of the Numba kernel (single-threaded, as the reference's), scaled by the
+    canonical per-leapfrog call counts (fp_p = 3 -> 5 traces + 5 W1, one W2,
+    fp_q = 3 Hessians + Psi^T H Psi + Psi Q, 5/3 sweeps per warm decomposition).
+    Returns (seconds per leapfrog, parts dict)."""
+    import oracle
+
+    model, data = workload_c4()
+    ot = oracle.OTarget(model, data)
+    d = ot.dim
+    rng = np.random.default_rng(7)
+    parts = {"hessian": [], "trace": [], "gemm": [], "rotation": []}
+    w = rng.standard_normal((d, d))
+    w = 0.5 * (w + w.T)
+    psi = rng.standard_normal((d, d))
+    for _ in range(reps):
+        q = 0.01 * rng.standard_normal(d)
+        pt = ot.at(q)
+        t0 = time.perf_counter()
+        h = pt.hessian()
+        parts["hessian"].append(time.perf_counter() - t0)
+        t0 = time.perf_counter()
+        pt.trace(w)
+        parts["trace"].append(time.perf_counter() - t0)
+        t0 = time.perf_counter()
+        _ = psi.T @ h
+        parts["gemm"].append(time.perf_counter() - t0)
+        a = np.ascontiguousarray(0.5 * (h + h.T))
+        v = np.eye(d)
+        t0 = time.perf_counter()
+        nrot = oracle.jacobi_passes(a, v, 0, 24, 0.0)
+        parts["rotation"].append((time.perf_counter() - t0) / max(1, nrot))
+    t = {k: float(np.median(v)) for k, v in parts.items()}
+    sweep = t["rotation"] * d * (d - 1) / 2
+    fp_p, fp_q, s = 3, 3, 5.0 / 3.0
+    n_tr = fp_p + 2
+    per_lf = n_tr * (t["trace"] + 2 * t["gemm"]) + t["gemm"] + fp_q * (t["hessian"] + 3 * t["gemm"] + s * sweep)
+    t["sweep"] = sweep
+    return per_lf, t
 
 
 # ---------------------------------------------------------------------------
@@ -108,10 +175,43 @@ class CpuPool:
         self.pool.join()
 
 
+def run_reference_c4(args):
+    """--impl reference at C4: each step is one bounded sample of the reference algorithm's
+    leapfrog on all host cores (cpu_c4_sample), reported in the GPU arm's units."""
+    cores = os.cpu_count() or 1
+    for _ in range(args.warmup):
+        cpu_c4_sample()
+    per_lf = []
+    t_all = 0.0
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        s_lf, parts = cpu_c4_sample()
+        t_all += time.perf_counter() - t0
+        per_lf.append(s_lf)
+    value = 1.0 / float(np.median(per_lf))
+    sample = (f"per step: 1 Hessian + 1 structured trace + 1 d^3 GEMM (numpy/OpenBLAS, {cores} threads) and "
+              f"24 passes (~{24 * 2082} rotations) of a cyclic Jacobi sweep (C restatement of the Numba "
+              f"kernel, 1 thread), scaled to one leapfrog by the SURVEY.md 8(d) call counts")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_all / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (reference generator simulate_meanvar(34, 19, n=8192, seed=0))",
+        "config": {"workload": C4_NAME, "chains": 1, "s_per_leapfrog_estimate": float(np.median(per_lf)),
+                   "parts_s": parts},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
 def run_reference(args):
     """--impl reference: the reference algorithm on all host cores."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
+        return
+    if args.workload == "c4":
+        run_reference_c4(args)
         return
     cores = os.cpu_count() or 1
     # each step: every core runs one chain for `lf` leapfrogs (bounded sample)
@@ -131,8 +231,7 @@ def run_reference(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total_t / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (reference generator simulate_logistic(1, n=512, seed=0))",
-        "config": {"workload": "C2 logistic GP classification N=512 d=34, eps=1e-3, C=100",
-                   "chains": cores, "leapfrogs_per_step_per_chain": lf},
+        "config": {"workload": C2_NAME, "chains": cores, "leapfrogs_per_step_per_chain": lf},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
                          "sample": f"{cores} processes x {lf} generalized leapfrogs per step "
                                    f"(oracle port, OPENBLAS_NUM_THREADS=1)"},
@@ -240,6 +339,196 @@ def measure_ess(target, sm_count, args, torch):
             "pilot_wall_s": wall}
 
 
+def _dist_setup():
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    # one rank per GPU; the modulo only matters for functional runs of several
+    # ranks on a one-GPU box (SGP_DIST_BACKEND=gloo), never for measurements
+    dev_index = local % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(dev_index)
+    if world > 1:
+        backend = os.environ.get("SGP_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev_index))
+        else:
+            dist.init_process_group(backend)
+    return torch, dist, world, rank, dev_index
+
+
+def count_kernel_launches(torch, fn):
+    """Kernels launched by fn() (CUPTI activity records through torch.profiler), untimed."""
+    from torch.profiler import ProfilerActivity, profile
+
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        fn()
+        torch.cuda.synchronize()
+    names = {}
+    for ev in prof.events():
+        if getattr(ev, "device_type", None) is not None and str(ev.device_type).endswith("CUDA"):
+            n = ev.name
+            if n.startswith(("Memcpy", "Memset", "cudaMemcpy", "cudaMemset")):
+                continue
+            names[n] = names.get(n, 0) + 1
+    return sum(names.values()), names
+
+
+def run_gpu_c4(args):
+    """C4: one chain per GPU (replicas), one MH move of C leapfrogs per step."""
+    torch, dist, world, rank, dev_index = _dist_setup()
+    from paper_2511_06407_b200.posterior import PosteriorTarget
+    from paper_2511_06407_b200.sampler import ChainConfig, DeviceChains
+
+    model, data = workload_c4()
+    target = PosteriorTarget(model, data)
+    d = target.dim
+    C = args.leapfrogs or C4_LEAPFROGS
+    cfg = ChainConfig(epsilon=C4_EPS, leapfrogs=C, moves=1, burnin=0, warm_order=args.warm_order or "parallel",
+                      cold_order="cyclic")
+    Z = 1
+    chains = DeviceChains(target.device, np.ones(Z), cfg)
+    chains.set_q(np.zeros((Z, d)))
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    chains.init()
+    st0 = chains.status_host()
+    cold_s = time.perf_counter() - t0
+    if np.count_nonzero(st0):
+        raise RuntimeError(f"chain start failed (status {st0})")
+    rng = np.random.default_rng([rank, 4])
+
+    def draws():
+        z = rng.standard_normal((1, Z, d))
+        with np.errstate(divide="ignore"):
+            lu = np.log(rng.uniform(size=(1, Z)))
+        return z, lu
+
+    n_dev = args.warmup + args.steps
+    dev_in = [tuple(torch.from_numpy(a).cuda() for a in draws()) for _ in range(n_dev)]
+    stream = torch.cuda.current_stream()
+    for w in range(args.warmup):
+        chains.run(1, *dev_in[w], move_offset=w)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    times = []
+    accepted = []
+    with ClockSampler(dev_index) as clocks:
+        t_wall = time.perf_counter()
+        for k in range(args.steps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            b = chains.run(1, *dev_in[args.warmup + k], move_offset=args.warmup + k)
+            e1.record(stream)
+            times.append((e0, e1))
+            accepted.append(b["accept"].clone())
+        torch.cuda.synchronize()
+        t_wall = time.perf_counter() - t_wall
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    status = chains.status_host()
+    if np.count_nonzero(status):
+        raise RuntimeError(f"chain stopped during the timed region (status {status}): no valid throughput")
+    dev_s = sum(a.elapsed_time(b) for a, b in times) / 1e3
+    acc = float(torch.stack(accepted).float().mean().item())
+    t_max = torch.tensor([dev_s], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
+    T = float(t_max.item())
+    total_lf = world * Z * C * args.steps
+    value = total_lf / T
+
+    # ---- e2e: host RNG draws -> pinned H2D -> the move -> D2H of records and position
+    zpin = torch.empty((1, Z, d), dtype=torch.float64).pin_memory()
+    lpin = torch.empty((1, Z), dtype=torch.float64).pin_memory()
+    rec_pin = {k: torch.empty((1, Z), dtype=torch.float64).pin_memory()
+               for k in ("logpost", "h_before", "h_after", "sweeps_mean")}
+    acc_pin = torch.empty((1, Z), dtype=torch.uint8).pin_memory()
+    q_pin = torch.empty((Z, d), dtype=torch.float64).pin_memory()
+    e2e_steps = max(1, min(args.steps, args.e2e_steps))
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for k in range(e2e_steps):
+        z, lu = draws()
+        zpin.numpy()[...] = z
+        lpin.numpy()[...] = lu
+        b = chains.run(1, zpin.to("cuda", non_blocking=True), lpin.to("cuda", non_blocking=True),
+                       move_offset=n_dev + k)
+        for k2, t in rec_pin.items():
+            t.copy_(b[k2], non_blocking=True)
+        acc_pin.copy_(b["accept"], non_blocking=True)
+        q_pin.copy_(chains.q, non_blocking=True)
+        torch.cuda.synchronize()
+    e2e_t = time.perf_counter() - t0
+    e2e_max = torch.tensor([e2e_t], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(e2e_max, op=dist.ReduceOp.MAX)
+    e2e_value = world * Z * C * e2e_steps / float(e2e_max.item())
+    h2d = Z * d * 8 + Z * 8
+    d2h = 4 * Z * 8 + Z + Z * d * 8
+
+    if rank == 0:
+        # kernels per move, counted on one extra (untimed) move
+        zc, lc = draws()
+        launches, names = count_kernel_launches(
+            torch, lambda: chains.run(1, zc, lc, move_offset=n_dev + e2e_steps))
+        Ds = c4_feature_widths(model)
+        F = canonical_flops_per_leapfrog(model_rows(data), Ds, d)
+        achieved = F * C * args.steps / dev_s / 1e12
+        dgemm = measure_dgemm_tflops(torch)
+        top = sorted(names.items(), key=lambda kv: -kv[1])[:8]
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * T / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (reference generator simulate_meanvar(34, 19, n=8192, seed=0))",
+            "config": {"workload": C4_NAME, "chains_per_gpu": Z, "leapfrogs_per_move": C,
+                       "step": f"one MH move ({C} generalized leapfrogs) of the chain",
+                       "warm_order": cfg.warm_order, "cold_order": cfg.cold_order,
+                       "parallelism": f"replicas x{world} (one chain per GPU)",
+                       "l2": "inputs (Phi 136 MB + the d x d working set) exceed L2; no flush",
+                       "acceptance": acc, "cold_init_s": cold_s,
+                       "per_chain_leapfrogs_per_s": value / (world * Z),
+                       "ms_per_leapfrog": 1e3 * T / (C * args.steps)},
+            "gpu_launches": launches * args.steps,
+            "gpu_launches_per_move": launches, "gpu_launch_top": top,
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "steps": e2e_steps},
+            "roofline": {"bound": "tensor", "achieved": achieved, "peak": dgemm, "unit": "TFLOP/s",
+                         "frac": achieved / dgemm, "traffic": None,
+                         "kernel": "whole generalized leapfrog (DMMA GEMMs + block Jacobi + glue)",
+                         "flops_per_leapfrog": F,
+                         "flops_source": "SURVEY.md 8(d) canonical count (fp_p=3, fp_q=3, s=5/3)",
+                         "peak_source": "cuBLAS DGEMM 8192^3 measured in this run (FP64 tensor pipe; "
+                                        "MEASURED_PEAKS.json has no FP64 entry)"},
+            "clocks": clocks.summary(),
+            "wall_s_timed": t_wall,
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            s_lf, parts = cpu_c4_sample()
+            cores = os.cpu_count() or 1
+            line["cpu_baseline"] = {
+                "value": 1.0 / s_lf, "unit": UNIT, "cores": cores, "kind": "port",
+                "sample": "1 Hessian + 1 structured trace + 1 d^3 GEMM (numpy/OpenBLAS, all threads) and 24 passes "
+                          "of a cyclic Jacobi sweep (C restatement of the Numba kernel, 1 thread), scaled to one "
+                          "leapfrog by the SURVEY.md 8(d) call counts",
+                "parts_s": parts}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def model_rows(data):
+    return int(np.asarray(data.y).shape[0])
+
+
 def run_gpu(args):
     import torch
     import torch.distributed as dist
@@ -296,7 +585,7 @@ def run_gpu(args):
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
     stream = torch.cuda.current_stream()
     for w in range(args.warmup):
-        chains.run(1, zs_all[w], lu_all[w])
+        chains.run(1, zs_all[w], lu_all[w], move_offset=w)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -308,7 +597,7 @@ def run_gpu(args):
             flush.fill_(float(k))  # evict L2 between timed steps (untimed)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            chains.run(1, zs_all[args.warmup + k], lu_all[args.warmup + k])
+            chains.run(1, zs_all[args.warmup + k], lu_all[args.warmup + k], move_offset=args.warmup + k)
             e1.record(stream)
             times.append((e0, e1))
         torch.cuda.synchronize()
@@ -318,6 +607,9 @@ def run_gpu(args):
     torch.cuda.synchronize()
     dev_s = sum(a.elapsed_time(b) for a, b in times) / 1e3
     status = chains.status_host()
+    if np.count_nonzero(status):
+        raise RuntimeError(f"{np.count_nonzero(status)} chains stopped (status != 0): throughput would count "
+                           "leapfrogs that were not run")
     bufs = chains._rec[1]
     acc = float(bufs["accept"].float().mean().item())
     sweeps = float(bufs["sweeps_mean"].mean().item())
@@ -340,13 +632,13 @@ def run_gpu(args):
     torch.cuda.synchronize()
     e2e_steps = max(1, args.steps)
     t0 = time.perf_counter()
-    for _ in range(e2e_steps):
+    for k in range(e2e_steps):
         z, lu = draws()
         zpin.numpy()[...] = z
         lpin.numpy()[...] = lu
         zd = zpin.to("cuda", non_blocking=True)
         ld = lpin.to("cuda", non_blocking=True)
-        b = chains.run(1, zd, ld)
+        b = chains.run(1, zd, ld, move_offset=args.warmup + args.steps + k)
         for k2, t in out_pin.items():
             t.copy_(b[k2], non_blocking=True)
         acc_pin.copy_(b["accept"], non_blocking=True)
@@ -366,7 +658,7 @@ def run_gpu(args):
 
     if rank == 0:
         N, D = N_ROWS, d - 3
-        F = canonical_flops_per_leapfrog(N, D, d, s=max(1.0, sweeps))
+        F = canonical_flops_per_leapfrog(N, (D,), d, s=max(1.0, sweeps))
         achieved = F * Z * LEAPFROGS * args.steps / dev_s / 1e12
         dgemm = measure_dgemm_tflops(torch)
         peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
@@ -375,7 +667,7 @@ def run_gpu(args):
             "warmup": args.warmup, "ms_per_step": 1e3 * T / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (reference generator simulate_logistic(1, n=512, seed=0))",
-            "config": {"workload": "C2 logistic GP classification N=512 d=34, eps=1e-3, C=100",
+            "config": {"workload": C2_NAME,
                        "chains_per_gpu": Z, "step": "one MH move (100 generalized leapfrogs) per chain",
                        "warm_order": args.warm_order, "parallelism": f"replicas x{world}",
                        "l2": "flushed between steps (256 MiB write, untimed)",
@@ -429,9 +721,13 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="c4", choices=["c4", "c2"])
+    ap.add_argument("--leapfrogs", type=int, default=0, help="leapfrogs per move (C4 default 100)")
+    ap.add_argument("--e2e-steps", type=int, default=3, help="moves timed end to end (C4)")
     ap.add_argument("--chains", type=int, default=0, help="chains per GPU (default SMs x chains-per-sm)")
     ap.add_argument("--chains-per-sm", type=int, default=12)
-    ap.add_argument("--warm-order", default="cyclic", choices=["cyclic", "parallel"])
+    ap.add_argument("--warm-order", default=None, choices=["cyclic", "parallel"],
+                    help="warm eigensolver order (C4 default parallel, C2 default cyclic)")
     ap.add_argument("--ref-leapfrogs", type=int, default=20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ess-moves", type=int, default=300, help="recorded moves of the min-ESS pilot (0: skip)")
@@ -440,7 +736,10 @@ def main():
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
+    elif args.workload == "c4":
+        run_gpu_c4(args)
     else:
+        args.warm_order = args.warm_order or "cyclic"
         run_gpu(args)
 
 

@@ -62,6 +62,9 @@ def _native():
         lib.oracle_jacobi_sweeps.restype = ctypes.c_long
         lib.oracle_jacobi_sweeps.argtypes = [dp, dp, ctypes.c_long, ctypes.c_double,
                                              ctypes.c_double, ctypes.c_long]
+        lib.oracle_jacobi_passes.restype = ctypes.c_long
+        lib.oracle_jacobi_passes.argtypes = [dp, dp, ctypes.c_long, ctypes.c_long, ctypes.c_long,
+                                             ctypes.c_double]
         lib.oracle_mgs.restype = None
         lib.oracle_mgs.argtypes = [dp, ctypes.c_long]
         lib.oracle_off_norm.restype = ctypes.c_double
@@ -79,6 +82,12 @@ def jacobi_sweeps(a, v, tol, skip, max_sweeps):
     assert a.flags.c_contiguous and v.flags.c_contiguous
     return int(_native().oracle_jacobi_sweeps(_ptr(a), _ptr(v), a.shape[0], tol, skip,
                                               max_sweeps))
+
+
+def jacobi_passes(a, v, p0, p1, skip):
+    """Passes p0..p1-1 of one cyclic sweep (timing samples only); returns rotations applied."""
+    assert a.flags.c_contiguous and v.flags.c_contiguous
+    return int(_native().oracle_jacobi_passes(_ptr(a), _ptr(v), a.shape[0], p0, p1, skip))
 
 
 def modified_gram_schmidt(psi):

@@ -71,6 +71,51 @@ long oracle_jacobi_sweeps(double *a, double *v, long d, double tol, double skip,
     }
 }
 
+/* Passes p0 .. p1-1 of one cyclic sweep (the body of _jacobi.py:54-85 for those pivot rows);
+ * returns the number of rotations applied.  Used only to time a bounded sample of a sweep for
+ * the CPU baseline at large d (bench.py); a full sweep is passes 0 .. d-2. */
+long oracle_jacobi_passes(double *a, double *v, long d, long p0, long p1, double skip)
+{
+    long nrot = 0;
+    for (long p = p0; p < p1 && p + 1 < d; ++p) {
+        for (long q = p + 1; q < d; ++q) {
+            const double apq = a[p * d + q];
+            if (fabs(apq) <= skip) continue;
+            const double theta = (a[q * d + q] - a[p * d + p]) / (2.0 * apq);
+            double t;
+            if (fabs(theta) > 1e154)
+                t = 0.5 / theta;
+            else if (theta >= 0.0)
+                t = 1.0 / (theta + sqrt(1.0 + theta * theta));
+            else
+                t = -1.0 / (-theta + sqrt(1.0 + theta * theta));
+            const double c = 1.0 / sqrt(1.0 + t * t);
+            const double s = t * c;
+            a[p * d + p] -= t * apq;
+            a[q * d + q] += t * apq;
+            a[p * d + q] = 0.0;
+            a[q * d + p] = 0.0;
+            for (long k = 0; k < d; ++k) {
+                if (k == p || k == q) continue;
+                const double akp = a[k * d + p];
+                const double akq = a[k * d + q];
+                a[k * d + p] = c * akp - s * akq;
+                a[p * d + k] = a[k * d + p];
+                a[k * d + q] = s * akp + c * akq;
+                a[q * d + k] = a[k * d + q];
+            }
+            for (long k = 0; k < d; ++k) {
+                const double vkp = v[k * d + p];
+                const double vkq = v[k * d + q];
+                v[k * d + p] = c * vkp - s * vkq;
+                v[k * d + q] = s * vkp + c * vkq;
+            }
+            ++nrot;
+        }
+    }
+    return nrot;
+}
+
 void oracle_mgs(double *psi, long d)
 {
     for (long i = 0; i < d; ++i) {
