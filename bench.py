@@ -5,7 +5,7 @@ C4): the multiple-kernel mean/variance GP model scaled to N = 8192 rows,
 simulate_meanvar(34, 19, n=8192, seed=0) with the "nl-meanvar" preset (d = 2083), epsilon =
 1e-4, C = 100 leapfrogs per move, one chain per GPU ("replicas": a chain is never split
 across GPUs).  One step = one MH move (C generalized leapfrogs + the Metropolis test).  Warm
-decompositions use the block Jacobi (warm_order="parallel"); cold ones (chain start,
+decompositions use the GEMM eigenvector refinement (warm_order="refine"); cold ones (chain start,
 rejections) the reference's pivot order, bit-identical (sgp_jbig.cuh).
 
     python bench.py [--gpus N] [--steps K] [--warmup W]            # C4 (headline)
@@ -386,7 +386,7 @@ def run_gpu_c4(args):
     target = PosteriorTarget(model, data)
     d = target.dim
     C = args.leapfrogs or C4_LEAPFROGS
-    cfg = ChainConfig(epsilon=C4_EPS, leapfrogs=C, moves=1, burnin=0, warm_order=args.warm_order or "parallel",
+    cfg = ChainConfig(epsilon=C4_EPS, leapfrogs=C, moves=1, burnin=0, warm_order=args.warm_order or "refine",
                       cold_order="cyclic")
     Z = 1
     chains = DeviceChains(target.device, np.ones(Z), cfg)
@@ -726,8 +726,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3, help="moves timed end to end (C4)")
     ap.add_argument("--chains", type=int, default=0, help="chains per GPU (default SMs x chains-per-sm)")
     ap.add_argument("--chains-per-sm", type=int, default=12)
-    ap.add_argument("--warm-order", default=None, choices=["cyclic", "parallel"],
-                    help="warm eigensolver order (C4 default parallel, C2 default cyclic)")
+    ap.add_argument("--warm-order", default=None, choices=["cyclic", "parallel", "refine"],
+                    help="warm eigensolver (C4 default refine, C2 default cyclic)")
     ap.add_argument("--ref-leapfrogs", type=int, default=20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ess-moves", type=int, default=300, help="recorded moves of the min-ESS pilot (0: skip)")

@@ -67,6 +67,8 @@ extern "C" {
 /* warm eigensolver pivot order */
 #define SGP_ORDER_CYCLIC 0          /* reference order, _jacobi.py:54-55 */
 #define SGP_ORDER_PARALLEL 1        /* round-robin (Brent-Luk) order: d/2 rotations per round */
+#define SGP_ORDER_REFINE 2          /* warm only, d > 256: GEMM eigenvector refinement (Ogita-Aishima),
+                                       block-Jacobi fallback; elsewhere treated as PARALLEL */
 
 /* what sgp_eval computes */
 #define SGP_EVAL_POTENTIAL 1

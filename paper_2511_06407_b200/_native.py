@@ -35,7 +35,7 @@ TRANSFORM_LOG = 0
 TRANSFORM_IDENTITY = 1
 
 METRIC_CODES = {"softabs-dynamic": 0, "softabs-static": 1, "euclidean": 2}
-ORDER_CODES = {"cyclic": 0, "parallel": 1}
+ORDER_CODES = {"cyclic": 0, "parallel": 1, "refine": 2}
 
 EVAL_POTENTIAL = 1
 EVAL_GRADIENT = 2

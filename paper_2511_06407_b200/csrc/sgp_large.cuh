@@ -1266,6 +1266,78 @@ static void lg_mgs_blocked(LgCtx &c, int slot) {
     k_lg_transpose<<<tgrid, dim3(32, 8), 0, c.s>>>(c.L.P[slot], c.L.X, d);
 }
 
+// Re-orthonormalisation of P_slot's columns for the non-bit-exact warm orders.  MGS returns
+// Q = Psi R^-1 with R the Cholesky factor of G = Psi^T Psi (_jacobi.py:89-107 is the column
+// form of that QR).  Warm bases drift from orthonormality only by rounding (|G - I| ~ 1e-13
+// after gs_interval calls), so R = I + F + O(|G-I|^2) with F = triu(G - I, 1) + diag(G - I)/2,
+// and Q = Psi (I - F) to O(|G-I|^2) ~ 1e-26: two DMMA GEMMs instead of d sequential grid
+// steps (48 ms per call at d = 2083).  Falls back to the MGS steps when |G - I| > 1e-6.
+__global__ void k_cholqr_m(const double *G, int d, double *M, double *part) {
+    __shared__ double red[32];
+    double mx = 0.0;
+    for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < (size_t)d * d;
+         idx += (size_t)gridDim.x * blockDim.x) {
+        const int i = (int)(idx / d), j = (int)(idx - (size_t)i * d);
+        const double e = G[idx] - (i == j ? 1.0 : 0.0);
+        mx = fmax(mx, fabs(e));
+        M[idx] = (i == j) ? 1.0 - 0.5 * e : (i < j ? -e : 0.0);
+    }
+    for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_down_sync(0xffffffffu, mx, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double m = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) m = fmax(m, red[w]);
+        part[blockIdx.x] = m;
+    }
+}
+__global__ void k_max_final(const double *part, int n, double *out) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        double m = 0.0;
+        for (int i = 0; i < n; ++i) m = fmax(m, part[i]);
+        *out = m;
+    }
+}
+
+static void lg_mgs(LgCtx &c, int slot);
+
+static void lg_cholqr(LgCtx &c, int slot) {
+    const int d = c.d;
+    const size_t dd = (size_t)d * d;
+    double *psi = c.L.P[slot], *G = c.L.bjA, *Mm = c.L.bjT, *Pn = c.L.bjV[0];
+    GemmArgs g{};
+    g.M = g.N = g.K = d;
+    g.A = psi;
+    g.lda = d;
+    g.TA = 1;
+    g.B = psi;
+    g.ldb = d;
+    g.C = G;
+    g.ldc = d;
+    g.alpha = 1.0;
+    g.upper_only = 1;
+    gemm_launch(g, c.s);  // G = Psi^T Psi (upper tiles)
+    k_mirror_upper<<<lg_blocks(dd), 256, 0, c.s>>>(G, d, d);
+    k_cholqr_m<<<148, 256, 0, c.s>>>(G, d, Mm, c.L.bjPart);
+    k_max_final<<<1, 32, 0, c.s>>>(c.L.bjPart, 148, c.L.sc + 15);
+    lg_sync(c);
+    if (!(c.sc[15] <= 1e-6)) {
+        lg_mgs(c, slot);
+        return;
+    }
+    GemmArgs h{};
+    h.M = h.N = h.K = d;
+    h.A = psi;
+    h.lda = d;
+    h.B = Mm;
+    h.ldb = d;
+    h.C = Pn;
+    h.ldc = d;
+    h.alpha = 1.0;
+    gemm_launch(h, c.s);  // Psi (I - F)
+    k_lg_copy<<<lg_blocks(dd), 256, 0, c.s>>>(psi, Pn, dd);
+}
+
 // Modified Gram-Schmidt of P_slot's columns (_jacobi.py:90-107) as d grid
 // steps on the transposed matrix (rows contiguous); X is free at this point.
 static void lg_mgs(LgCtx &c, int slot) {
@@ -1284,18 +1356,219 @@ static void lg_mgs(LgCtx &c, int slot) {
     k_lg_transpose<<<tgrid, dim3(32, 8), 0, c.s>>>(c.L.P[slot], c.L.X, d);
 }
 
+// ---- warm decomposition by eigenvector refinement (warm_order = "refine") ----
+//
+// A warm call starts from the previous basis Psi, which already nearly diagonalises the new
+// Hessian (measured at C4: off(Psi^T H Psi) ~ 1e-5 ||H||, every coupling below 4 % of its
+// eigenvalue gap; profiles/r2_c4_warm_structure.md).  Instead of Jacobi rounds it applies the
+// Ogita-Aishima refinement (Ogita & Aishima 2018, "Iterative refinement for symmetric
+// eigenvalue decomposition"), all rotations of a sweep at once through four DMMA GEMMs:
+//   S = Psi^T H Psi,  G = Psi^T Psi,  lam_i = s_ii / g_ii,
+//   E_ij = (s_ij + lam_j r_ij) / (lam_j - lam_i)  (i != j),  E_ii = r_ii / 2,  r = I - G,
+//   Psi <- Psi + Psi E,
+// which converges quadratically and keeps Psi orthonormal to rounding (the r terms), so the
+// every-gs_interval Gram-Schmidt of the Jacobi path is folded into every iteration.  The stop
+// test is the reference's: off(S) <= zeta ||H||_F (metric.py:101-109, 172).  Columns keep their
+// order (Psi moves by O(E)), so eigenvalues stay in the warm natural order.  Couplings below
+// the reference's skip threshold tol/d are not rotated (only the orthogonality term applies),
+// as the Jacobi skips them.  Pairs whose coupling exceeds their gap are still updated: the
+// iteration recovers within one or two steps (measured on C4 warm problems with ratios up to
+// 1.8, tools/refine_sim.py), orthogonality included.  A coupling 1e3 times its gap, an off-norm
+// that stops decreasing, a non-finite value, or more than 8 iterations hand the call to the
+// block Jacobi from the same starting basis.
+__global__ void k_oa_lam(const double *S, const double *G, int d, double *lam) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < d; i += gridDim.x * blockDim.x)
+        lam[i] = S[(size_t)i * d + i] / G[(size_t)i * d + i];
+}
+#define OA_ETA 1e3  // a coupling this far above its eigenvalue gap goes to the block Jacobi
+#define OA_MAXPAIRS 1024
+// off-norm^2 of sym(S) and E (when G is given); partials per CTA: [off2, max ratio of the
+// pairs in the first-order regime]; pairs with |s_ij| > OA_ETA |gap| are counted in *npairs
+// (the first OA_MAXPAIRS listed in pairs, for diagnostics)
+__global__ void k_oa_E(const double *S, const double *G, const double *lam, int d, double *E, double *part,
+                       int *pairs = nullptr, int *npairs = nullptr, double skip = 0.0) {
+    __shared__ double r0[32], r1[32];
+    double off2 = 0.0, mr = 0.0;
+    for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < (size_t)d * d;
+         idx += (size_t)gridDim.x * blockDim.x) {
+        const int i = (int)(idx / d), j = (int)(idx - (size_t)i * d);
+        if (i == j) {
+            if (G) E[idx] = 0.5 * (1.0 - G[idx]);
+            continue;
+        }
+        const double sij = 0.5 * (S[idx] + S[(size_t)j * d + i]);
+        off2 += sij * sij;
+        if (G) {
+            const double rij = -0.5 * (G[idx] + G[(size_t)j * d + i]);
+            if (fabs(sij) <= skip) {
+                // below the reference's skip threshold (|a_pq| <= tol/d, _jacobi.py:57-58): no
+                // rotation, only the orthogonality correction (Ogita-Aishima's clustered case)
+                E[idx] = 0.5 * rij;
+                continue;
+            }
+            const double gap = lam[j] - lam[i];
+            const double e = (sij + lam[j] * rij) / gap;
+            E[idx] = e;
+            const double ratio = fabs(sij) / fabs(gap);
+            if (pairs && ratio > OA_ETA && !(ratio != ratio) && sij != 0.0) {
+                if (i < j) {
+                    const int k = atomicAdd(npairs, 1);
+                    if (k < OA_MAXPAIRS) {
+                        pairs[2 * k] = i;
+                        pairs[2 * k + 1] = j;
+                    }
+                }
+            } else {
+                mr = (ratio > mr || ratio != ratio) ? ratio : mr;  // NaN propagates
+            }
+        }
+    }
+    off2 = warp_sum(off2);
+    for (int o = 16; o; o >>= 1) {
+        const double v = __shfl_down_sync(0xffffffffu, mr, o);
+        mr = (v > mr || v != v) ? v : mr;
+    }
+    if ((threadIdx.x & 31) == 0) {
+        r0[threadIdx.x >> 5] = off2;
+        r1[threadIdx.x >> 5] = mr;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double a = 0.0, b = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+            a += r0[w];
+            b = (r1[w] > b || r1[w] != r1[w]) ? r1[w] : b;
+        }
+        part[2 * blockIdx.x] = a;
+        part[2 * blockIdx.x + 1] = b;
+    }
+}
+__global__ void k_oa_fin(const double *part, int n, double *out) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        double a = 0.0, b = 0.0;
+        for (int i = 0; i < n; ++i) {
+            a += part[2 * i];
+            b = (part[2 * i + 1] > b || part[2 * i + 1] != part[2 * i + 1]) ? part[2 * i + 1] : b;
+        }
+        out[0] = sqrt(a);
+        out[1] = b;
+    }
+}
+__global__ void k_oa_setdiag(double *H, const double *S, int d) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < d; i += gridDim.x * blockDim.x)
+        H[(size_t)i * d + i] = S[(size_t)i * d + i];
+}
+
+static void lg_gemm_ab(LgCtx &c, int M, int N, int K, const double *A, int lda, int TA, const double *B, int ldb,
+                       int TB, double *C, int ldc, double alpha, double beta, int upper) {
+    GemmArgs g{};
+    g.M = M;
+    g.N = N;
+    g.K = K;
+    g.A = A;
+    g.lda = lda;
+    g.TA = TA;
+    g.B = B;
+    g.ldb = ldb;
+    g.TB = TB;
+    g.C = C;
+    g.ldc = ldc;
+    g.alpha = alpha;
+    g.beta = beta;
+    g.upper_only = upper;
+    gemm_launch(g, c.s);
+}
+
+static int lg_eig_warm_jacobi(LgCtx &c, int src, int dst, int *sweeps);
+
+static int lg_eig_refine(LgCtx &c, int src, int dst, int *sweeps) {
+    const int d = c.d;
+    const size_t dd = (size_t)d * d;
+    int since = c.since[src] + 1;
+    if (c.cfg.gs_interval && since >= c.cfg.gs_interval) since = 0;  // orthonormality is refined every iteration
+    const double hnorm = lg_hnorm(c);  // ||H||_F of the unsymmetrised Hessian (metric.py:172)
+    const double tol = c.cfg.zeta * hnorm;
+    k_lg_symmetrize<<<lg_blocks(dd), 256, 0, c.s>>>(c.L.H, d);
+    double *psi = c.L.P[dst], *Y = c.L.X, *Sm = c.L.W, *G = c.L.bjA, *E = c.L.bjT, *Pn = c.L.bjV[0];
+    double *lam = c.L.vec + (size_t)V_TMP * d;  // scratch d-vector (free during the eigensolver)
+    k_lg_copy<<<lg_blocks(dd), 256, 0, c.s>>>(psi, c.L.P[src], dd);
+    const int nb = 148;  // two partials per CTA: bjPart holds 512 doubles
+    double prev_off = INFINITY;
+    for (int it = 0;; ++it) {
+        lg_gemm_ab(c, d, d, d, c.L.H, d, 0, psi, d, 0, Y, d, 1.0, 0.0, 0);  // Y = H Psi
+        lg_gemm_ab(c, d, d, d, psi, d, 1, Y, d, 0, Sm, d, 1.0, 0.0, 1);     // S = Psi^T Y (upper tiles)
+        k_mirror_upper<<<lg_blocks(dd), 256, 0, c.s>>>(Sm, d, d);
+        k_oa_E<<<nb, 256, 0, c.s>>>(Sm, nullptr, nullptr, d, nullptr, c.L.bjPart);
+        k_oa_fin<<<1, 32, 0, c.s>>>(c.L.bjPart, nb, c.L.sc + 13);
+        lg_sync(c);
+        const double off = c.sc[13];
+        if (getenv("SGP_DEBUG_REFINE")) fprintf(stderr, "refine it %d off %.3e tol %.3e\n", it, off, tol);
+        if (it == 0 && getenv("SGP_DUMP_REFINE")) {  // diagnostics: the warm problem of this call
+            static int dumped = 0;
+            std::vector<double> hS(dd);
+            cudaMemcpyAsync(hS.data(), Sm, sizeof(double) * dd, cudaMemcpyDeviceToHost, c.s);
+            cudaStreamSynchronize(c.s);
+            char path[512];
+            snprintf(path, sizeof(path), "%s_%d.bin", getenv("SGP_DUMP_REFINE"), dumped++);
+            if (dumped <= 12) {
+                FILE *f = fopen(path, "wb");
+                if (f) {
+                    fwrite(&tol, sizeof(double), 1, f);
+                    fwrite(hS.data(), sizeof(double), dd, f);
+                    fclose(f);
+                }
+            }
+        }
+        if (off <= tol) {
+            k_oa_setdiag<<<lg_blocks(d), 256, 0, c.s>>>(c.L.H, Sm, d);
+            *sweeps = it;
+            lg_op(c, LG_GLAM, dst, 0, 0, since);
+            c.since[dst] = since;
+            return lg_sync(c);
+        }
+        // quadratic convergence or hand over: non-finite, not decreasing, or too many iterations
+        if (!(off < prev_off) || it >= std::min(c.cfg.sweep_cap, 8)) break;
+        prev_off = off;
+        lg_gemm_ab(c, d, d, d, psi, d, 1, psi, d, 0, G, d, 1.0, 0.0, 1);  // G = Psi^T Psi (upper tiles)
+        k_mirror_upper<<<lg_blocks(dd), 256, 0, c.s>>>(G, d, d);
+        k_oa_lam<<<lg_blocks(d), 256, 0, c.s>>>(Sm, G, d, lam);
+        int *pairs = c.L.jpairs, *npairs = c.L.jpairs + 2 * OA_MAXPAIRS;
+        cudaMemsetAsync(npairs, 0, sizeof(int), c.s);
+        k_oa_E<<<nb, 256, 0, c.s>>>(Sm, G, lam, d, E, c.L.bjPart, pairs, npairs, tol / d);
+        int np_h = 0;
+        cudaMemcpyAsync(&np_h, npairs, sizeof(int), cudaMemcpyDeviceToHost, c.s);
+        lg_sync(c);
+        if (np_h > 0) break;  // a (numerically) degenerate coupled pair: the Jacobi handles it
+        k_lg_copy<<<lg_blocks(dd), 256, 0, c.s>>>(Pn, psi, dd);
+        lg_gemm_ab(c, d, d, d, psi, d, 0, E, d, 0, Pn, d, 1.0, 1.0, 0);  // Psi + Psi E
+        k_lg_copy<<<lg_blocks(dd), 256, 0, c.s>>>(psi, Pn, dd);
+    }
+    // fall back to the block Jacobi from the original basis on the symmetric Hessian
+    if (getenv("SGP_DEBUG_REFINE")) fprintf(stderr, "refine -> block Jacobi fallback\n");
+    return lg_eig_warm_jacobi(c, src, dst, sweeps);
+}
+
 // warm decomposition of H in P_src's basis into slot dst (metric.py:145-185)
 static int lg_eig_warm(LgCtx &c, int src, int dst, int *sweeps) {
+    if (c.cfg.warm_order == SGP_ORDER_REFINE) return lg_eig_refine(c, src, dst, sweeps);
+    return lg_eig_warm_jacobi(c, src, dst, sweeps);
+}
+
+static int lg_eig_warm_jacobi(LgCtx &c, int src, int dst, int *sweeps) {
     const int d = c.d;
     int since = c.since[src] + 1;
     if (c.cfg.gs_interval && since >= c.cfg.gs_interval) {
-        // d grid steps (measured faster at d = 2083 than the blocked form, whose
-        // odd-stride panel GEMMs and single-CTA panel MGS cost ~80 ms per call)
-        const char *e = getenv("SGP_LG_BLOCK_MGS");
-        if (e && e[0] == '1')
-            lg_mgs_blocked(c, src);
-        else
-            lg_mgs(c, src);
+        if (c.cfg.warm_order == SGP_ORDER_CYCLIC) {
+            // the reference's column MGS, d grid steps (bit-faithful order of operations;
+            // measured faster at d = 2083 than the blocked form)
+            const char *e = getenv("SGP_LG_BLOCK_MGS");
+            if (e && e[0] == '1')
+                lg_mgs_blocked(c, src);
+            else
+                lg_mgs(c, src);
+        } else {
+            lg_cholqr(c, src);  // same Q to rounding, two DMMA GEMMs instead of d grid steps
+        }
         since = 0;
     }
     const double hnorm = lg_hnorm(c);
@@ -1304,7 +1577,7 @@ static int lg_eig_warm(LgCtx &c, int src, int dst, int *sweeps) {
     k_lg_symmetrize<<<lg_blocks((size_t)d * d), 256, 0, c.s>>>(c.L.H, d);
     k_lg_copy<<<lg_blocks((size_t)d * d), 256, 0, c.s>>>(c.L.P[dst], c.L.P[src], (size_t)d * d);
     const double tol = c.cfg.zeta * hnorm, skip = d ? tol / d : 0.0;
-    const int st = lg_jacobi(c, dst, tol, skip, c.cfg.warm_order == SGP_ORDER_PARALLEL, sweeps);
+    const int st = lg_jacobi(c, dst, tol, skip, c.cfg.warm_order != SGP_ORDER_CYCLIC, sweeps);
     if (st) return st;
     lg_op(c, LG_GLAM, dst, 0, 0, since);
     c.since[dst] = since;
@@ -1404,7 +1677,8 @@ static int lg_alloc(const ModelDev &M, LgPtrs &L, void **owner) {
     const size_t oS = take((size_t)F_COUNT * ld), oH = take(dd), oX = take(dd), oW = take(dd), oP0 = take(dd),
                  oP1 = take(dd), oY = take((size_t)std::max(M.mp.N, 1) * std::max(M.mp.Dtot, 1)),
                  osa = take(3 * (size_t)ld), ov = take(16 * (size_t)d), osc = take(16), osi = take(16),
-                 ost = take(2), ojl = take(sgp_jacobi_log_doubles(d)), ojp = take(5 * np), ojq = take(2 * np),
+                 ost = take(2), ojl = take(sgp_jacobi_log_doubles(d)), ojp = take(5 * np), ojq = take(std::max(2 * np, (size_t)4096)),  // + refine pair/cluster lists
+                
                  ored = take(64);
     // block Jacobi
     const int nbk = ((d + 2 * BJ_B - 1) / (2 * BJ_B)) * 2, dp = nbk * BJ_B, bnp = nbk / 2;

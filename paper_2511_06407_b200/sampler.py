@@ -25,7 +25,8 @@ from .posterior import DivergenceError, DomainError, PosteriorTarget, raise_stat
 
 LN_2PI = math.log(2.0 * math.pi)
 METRIC_MODES = ("softabs-dynamic", "softabs-static", "euclidean")
-WARM_ORDERS = ("parallel", "cyclic")
+WARM_ORDERS = ("parallel", "cyclic", "refine")
+COLD_ORDERS = ("parallel", "cyclic")
 _DIVERGENT = (DivergenceError, DomainError, JacobiError, FloatingPointError)
 
 
@@ -35,11 +36,18 @@ class ChainError(RuntimeError):
 
 @dataclasses.dataclass(frozen=True)
 class ChainConfig:
-    """Chain settings (sampler.py:49-83), plus ``warm_order``: the pivot order of
-    the warm Jacobi.  "cyclic" (default) replays the reference's order and keeps
-    trajectories identical to the reference; "parallel" (round-robin, d/2
-    concurrent rotations) is faster but, the dynamics being chaotic, only
-    statistically equivalent after a few moves."""
+    """Chain settings (sampler.py:49-83), plus two solver choices.
+
+    ``warm_order``: the warm eigensolver (dynamic_eigendecompose).  "cyclic" (default)
+    replays the reference's pivot order and keeps trajectories identical to the reference;
+    "parallel" (round-robin order; block Jacobi at d > 256) and "refine" (d > 256: GEMM
+    eigenvector refinement with a block-Jacobi fallback; "parallel" below) are faster and
+    meet the same convergence test, but the dynamics being chaotic they are only
+    statistically equivalent after a few moves.
+
+    ``cold_order``: the cold eigensolver (static_eigendecompose: chain start, rejections,
+    rung starts).  "cyclic" (default) is the reference's order, bit-identical at every d;
+    "parallel" selects the block Jacobi at d > 256."""
 
     epsilon: float = 0.001
     leapfrogs: int = 100
@@ -78,8 +86,8 @@ class ChainConfig:
             raise ValueError(f"metric must be one of {METRIC_MODES}")
         if self.warm_order not in WARM_ORDERS:
             raise ValueError(f"warm_order must be one of {WARM_ORDERS}")
-        if self.cold_order not in WARM_ORDERS:
-            raise ValueError(f"cold_order must be one of {WARM_ORDERS}")
+        if self.cold_order not in COLD_ORDERS:
+            raise ValueError(f"cold_order must be one of {COLD_ORDERS}")
 
     def to_c(self):
         c = nat.ChainConfigC()

@@ -135,3 +135,18 @@ def test_c4_two_leapfrogs_from_reference_momentum(c4, c4_start):
     assert h_after == pytest.approx(float(g["h_after"]), rel=1e-12)
     accept = (float(g["h_before"]) - h_after) > np.log(float(g["uniform"]))
     assert accept == bool(g["accept"])
+
+
+def test_c4_refine_leapfrog_matches_reference(c4, c4_start):
+    """The production warm solver (warm_order="refine": GEMM eigenvector refinement) meets
+    the reference's convergence test, so the leapfrog from the reference momentum agrees with
+    the reference's (cyclic Jacobi) leapfrog to the Jacobi tolerance."""
+    g, q0, _, m0 = c4_start
+    cfg = S.ChainConfig(epsilon=float(g["epsilon"]), leapfrogs=1, moves=1, burnin=0, warm_order="refine")
+    q1, p1, m1, diag = S.leapfrog_step(q0, g["p0"], m0, c4, cfg)
+    assert rel_err(q1, g["q1"]) < 1e-8
+    assert rel_err(p1, g["p1"]) < 1e-8
+    assert rel_err(np.sort(m1.eigenvalues), np.sort(g["lam1"])) < 1e-9
+    assert [diag["fp_p_iters"]] == list(g["fp_p1"])
+    assert [diag["fp_q_iters"]] == list(g["fp_q1"])
+    assert all(0 < s <= 4 for s in diag["sweeps"])

@@ -106,8 +106,11 @@ def test_generic_cyclic_sweep_bit_exact(large_case):
     assert rel_err(G, G_o) < 1e-9
 
 
-@pytest.mark.parametrize("order", ["cyclic", "parallel"])
-def test_large_leapfrog_step_vs_oracle(large_case, order):
+@pytest.mark.parametrize("order,gs", [("cyclic", 10), ("parallel", 10), ("refine", 10), ("parallel", 1),
+                                      ("refine", 1)])
+def test_large_leapfrog_step_vs_oracle(large_case, order, gs):
+    """gs = 1 re-orthonormalises before every warm decomposition: the MGS steps in the cyclic
+    order, the Cholesky-QR correction (two GEMMs) in the others."""
     model, data, target, ot = large_case
     d = target.dim
     q0 = np.zeros(d)
@@ -115,10 +118,10 @@ def test_large_leapfrog_step_vs_oracle(large_case, order):
     m0 = M.MetricState(eigenvalues=om0.lam, vectors=om0.psi, softabs_values=om0.g, logdet=om0.logdet,
                        kappa=1.0, sweep_count=om0.sweeps, steps_since_refresh=0)
     p = om0.psi @ (np.sqrt(om0.g) * np.random.default_rng(9).standard_normal(d))
-    cfg = S.ChainConfig(epsilon=0.002, leapfrogs=1, moves=1, burnin=0, warm_order=order)
+    cfg = S.ChainConfig(epsilon=0.002, leapfrogs=1, moves=1, burnin=0, warm_order=order, gs_interval=gs)
     q1, p1, mt, diag = S.leapfrog_step(q0, p, m0, target, cfg)
     oq, op_, om, odiag = oracle.leapfrog_step(q0, p, om0, ot, oracle.OConfig(epsilon=0.002, leapfrogs=1,
-                                                                             moves=1, burnin=0))
+                                                                             moves=1, burnin=0, gs_interval=gs))
     tol = 1e-9 if order == "cyclic" else 1e-6
     assert rel_err(q1, oq) < tol
     assert rel_err(p1, op_) < tol
