@@ -503,7 +503,7 @@ def run_gpu_c4(args):
                     "steps": e2e_steps},
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": dgemm, "unit": "TFLOP/s",
                          "frac": achieved / dgemm, "traffic": None,
-                         "kernel": "whole generalized leapfrog (DMMA GEMMs + block Jacobi + glue)",
+                         "kernel": "whole generalized leapfrog (DMMA GEMMs: trace, Hessian, W, eigenvector refinement; glue)",
                          "flops_per_leapfrog": F,
                          "flops_source": "SURVEY.md 8(d) canonical count (fp_p=3, fp_q=3, s=5/3)",
                          "peak_source": "cuBLAS DGEMM 8192^3 measured in this run (FP64 tensor pipe; "

@@ -18,7 +18,7 @@ from paper_2511_06407_b200.sampler import ChainConfig, DeviceChains  # noqa: E40
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--leapfrogs", type=int, default=5)
-ap.add_argument("--order", default="parallel")
+ap.add_argument("--order", default="refine")
 ap.add_argument("--out", default=None)
 args = ap.parse_args()
 
