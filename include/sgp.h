@@ -252,7 +252,15 @@ typedef struct {
     double pinned_value[3];  /* their sampled-coordinate values (ln value for the log transform) */
     double gtol;
     int max_iters, memory;
+    int mode;                /* SGP_GRID_REFERENCE (default) or SGP_GRID_ROBUST */
 } sgp_grid_spec;
+/* SGP_GRID_REFERENCE: node k is (re)started from the optimum of the last node before it in
+ * serpentine order whose L-BFGS converged -- the reference's a_warm rule -- so the failure
+ * count (and the skip-tolerance RuntimeError) follows the reference.  SGP_GRID_ROBUST: nodes
+ * start from a = 0 and failures are retried warm-started; fewer failures than the reference
+ * (opt-in, documented as a deviation). */
+#define SGP_GRID_REFERENCE 0
+#define SGP_GRID_ROBUST 1
 int sgp_laplace_grid(const sgp_model *model, const sgp_grid_spec *spec, int n_nodes, double *h_values,
                      int *h_status, int *h_iters, void *stream);
 

@@ -95,7 +95,11 @@ class GridSpecC(ctypes.Structure):
     _fields_ = [("c_max", ctypes.c_double), ("c_mesh", ctypes.c_double), ("sigma_max", ctypes.c_double),
                 ("sigma_mesh", ctypes.c_double), ("n_pinned", ctypes.c_int),
                 ("pinned_pos", ctypes.c_int * 3), ("pinned_value", ctypes.c_double * 3),
-                ("gtol", ctypes.c_double), ("max_iters", ctypes.c_int), ("memory", ctypes.c_int)]
+                ("gtol", ctypes.c_double), ("max_iters", ctypes.c_int), ("memory", ctypes.c_int),
+                ("mode", ctypes.c_int)]
+
+
+GRID_MODES = {"reference": 0, "robust": 1}
 
 
 class MoveRecords(ctypes.Structure):

@@ -1075,13 +1075,52 @@ extern "C" int sgp_laplace_grid(const sgp_model *m, const sgp_grid_spec *spec, i
     for (int node0 = 0; !rc && node0 < n_nodes; node0 += batch) {
         const int nb = std::min(batch, n_nodes - node0);
         k_laplace_grid<<<nb, L.nt, L.pl.bytes, S(stream)>>>(m->dev, L.pl, gd, node0, n_nodes, d_scr, spc, stride,
-                                                             d_val, d_st, d_it, nullptr, nullptr, d_aopt);
+                                                             d_val, d_st, d_it, nullptr, nullptr, nullptr, d_aopt);
         rc = check_launch();
     }
-    // passes 2..: failed nodes again, warm-started from the optimum of the last
-    // converged node before them in serpentine order (the reference's a_warm)
     std::vector<int> st(n_nodes), list, src;
-    for (int pass = 0; !rc && pass < 4; ++pass) {
+    if (spec->mode == SGP_GRID_REFERENCE) {
+        // The reference's rule (evidence.py:374-403): node k starts from a_warm, the optimum of
+        // the last node before it in serpentine order whose L-BFGS converged (updated before the
+        // Cholesky test), 0 until the first one.  Its chain is sequential; here every node is
+        // re-run concurrently from the pass-1 optimum of that predecessor (the optimum a
+        // converged L-BFGS reaches does not depend on its start beyond gtol), so failures are
+        // counted for the reference's starting points and the skip tolerance keeps its meaning.
+        double *d_a1 = nullptr;
+        if (!rc && (cudaMemcpyAsync(st.data(), d_st, n_nodes * sizeof(int), cudaMemcpyDeviceToHost, S(stream)) !=
+                        cudaSuccess ||
+                    cudaStreamSynchronize(S(stream)) != cudaSuccess))
+            rc = SGP_ECUDA;
+        if (!rc && cudaMalloc(&d_a1, (size_t)n_nodes * d * sizeof(double)) != cudaSuccess) rc = SGP_ENOMEM;
+        if (!rc) {
+            cudaMemcpyAsync(d_a1, d_aopt, (size_t)n_nodes * d * sizeof(double), cudaMemcpyDeviceToDevice, S(stream));
+            int last = -1;
+            for (int k = 0; k < n_nodes; ++k) {
+                if (last >= 0) {  // nodes with no converged predecessor start at 0: pass 1 already is theirs
+                    list.push_back(k);
+                    src.push_back(last);
+                }
+                if (st[k] == 0 || st[k] == 2) last = k;
+            }
+            const int nl = (int)list.size();
+            if (nl) {
+                cudaMemcpyAsync(d_list, list.data(), nl * sizeof(int), cudaMemcpyHostToDevice, S(stream));
+                cudaMemcpyAsync(d_list + n_nodes, src.data(), nl * sizeof(int), cudaMemcpyHostToDevice, S(stream));
+            }
+            for (int node0 = 0; !rc && node0 < nl; node0 += batch) {
+                const int nb = std::min(batch, nl - node0);
+                k_laplace_grid<<<nb, L.nt, L.pl.bytes, S(stream)>>>(m->dev, L.pl, gd, node0, nl, d_scr, spc, stride,
+                                                                     d_val, d_st, d_it, d_list, d_list + n_nodes, d_a1,
+                                                                     d_aopt);
+                rc = check_launch();
+            }
+            cudaStreamSynchronize(S(stream));
+        }
+        cudaFree(d_a1);
+    }
+    // SGP_GRID_ROBUST passes 2..: failed nodes again, warm-started from the optimum of the
+    // last converged node before them in serpentine order (fewer failures than the reference)
+    for (int pass = 0; !rc && spec->mode != SGP_GRID_REFERENCE && pass < 4; ++pass) {
         if (cudaMemcpyAsync(st.data(), d_st, n_nodes * sizeof(int), cudaMemcpyDeviceToHost, S(stream)) != cudaSuccess ||
             cudaStreamSynchronize(S(stream)) != cudaSuccess) {
             rc = SGP_ECUDA;
@@ -1105,7 +1144,7 @@ extern "C" int sgp_laplace_grid(const sgp_model *m, const sgp_grid_spec *spec, i
         for (int node0 = 0; !rc && node0 < nl; node0 += batch) {
             const int nb = std::min(batch, nl - node0);
             k_laplace_grid<<<nb, L.nt, L.pl.bytes, S(stream)>>>(m->dev, L.pl, gd, node0, nl, d_scr, spc, stride, d_val,
-                                                                 d_st, d_it, d_list, d_list + n_nodes, d_aopt);
+                                                                 d_st, d_it, d_list, d_list + n_nodes, d_aopt, d_aopt);
             rc = check_launch();
         }
     }

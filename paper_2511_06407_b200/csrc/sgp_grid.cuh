@@ -280,13 +280,14 @@ __device__ __forceinline__ double inv_gamma_logpdf(double th, double a, double b
 // status: 0 ok, 1 optimiser did not converge, 2 Cholesky failed, 3 objective not
 // finite at the start (the reference raises ValueError there)
 // list == nullptr: nodes node0 + blockIdx.x (first pass, a = 0 starts);
-// else node = list[node0 + blockIdx.x] warm-started from the optimum of node
-// src[...] (the reference's serpentine a_warm, evidence.py:393-399).  The
-// optimum of every converged node is kept in aopt[node * d + i] (raw coefficients).
+// else node = list[node0 + blockIdx.x] warm-started from the optimum asrc of node
+// src[...] (the reference's serpentine a_warm, evidence.py:393-399; src < 0: a = 0).
+// The optimum of every node whose L-BFGS converged is kept in aopt[node * d + i]
+// (raw coefficients), before the Cholesky test, as the reference updates a_warm.
 __global__ void __launch_bounds__(SGP_MAX_NT) k_laplace_grid(ModelDev M, SmemPlan pl, GridDev gd, int node0,
                                                             int nodes, double *scratch, size_t spc, size_t stride,
                                                             double *val, int *status, int *iters, const int *list,
-                                                            const int *src, double *aopt) {
+                                                            const int *src, const double *asrc, double *aopt) {
     const int slot_id = node0 + blockIdx.x;
     if (slot_id >= nodes) return;
     const int node = list ? list[slot_id] : slot_id;
@@ -345,7 +346,7 @@ __global__ void __launch_bounds__(SGP_MAX_NT) k_laplace_grid(ModelDev M, SmemPla
     double *hist = my + spc;  // sgp_grid_scratch_extra(d, m) doubles
     double *Sh = hist, *Yh = hist + (size_t)m * d, *rho = hist + (size_t)2 * m * d, *alph = rho + m;
     double *sv = w.bv, *yv = w.tmp;  // candidate pair before acceptance
-    for (int i = threadIdx.x; i < n; i += SGP_NT) x[i] = from >= 0 ? aopt[(size_t)from * d + i] / scl[i] : 0.0;
+    for (int i = threadIdx.x; i < n; i += SGP_NT) x[i] = from >= 0 ? asrc[(size_t)from * d + i] / scl[i] : 0.0;
     __syncthreads();
     int it = 0;
     double f = 0.0;

@@ -327,11 +327,20 @@ class GridSpec:
         return c, s
 
 
-def laplace_grid_nodes(model, data, grid_spec=None, *, gtol=1e-6, max_iters=200, memory=10):
+def laplace_grid_nodes(model, data, grid_spec=None, *, gtol=1e-6, max_iters=200, memory=10, mode="reference"):
     """Per-node values of the grid oracle on the device, in the reference's
     serpentine node order: (values, status, iterations); status 0 ok,
     1 optimiser not converged, 2 Cholesky failed, 3 objective not finite at
-    the start.  Validation as evidence.py:341-366."""
+    the start.  Validation as evidence.py:341-366.
+
+    ``mode="reference"`` (default): every node starts from the optimum of the last node
+    before it in serpentine order whose L-BFGS converged -- the reference's a_warm rule
+    (evidence.py:374-399) -- evaluated concurrently from a first a = 0 pass, so failures are
+    counted at the reference's starting points.  ``mode="robust"`` (opt-in, differs from the
+    reference): a = 0 starts with warm-started retries of the failures, which leaves fewer
+    failed nodes (profiles/r1_laplace_grid.md)."""
+    if mode not in ("reference", "robust"):
+        raise ValueError("mode must be 'reference' or 'robust'")
     from . import _native as nat
 
     from .rrgp import BlockLayout
@@ -357,6 +366,7 @@ def laplace_grid_nodes(model, data, grid_spec=None, *, gtol=1e-6, max_iters=200,
         k += 1
     spec.n_pinned = k
     spec.gtol, spec.max_iters, spec.memory = float(gtol), int(max_iters), int(memory)
+    spec.mode = nat.GRID_MODES[mode]
     c_centers, s_centers = grid.centers()
     n = c_centers.size * s_centers.size
     target = PosteriorTarget(model, data)
@@ -369,17 +379,17 @@ def laplace_grid_nodes(model, data, grid_spec=None, *, gtol=1e-6, max_iters=200,
     return values, status, iters
 
 
-def laplace_grid_oracle(model, data, grid_spec=None, *, gtol=1e-6, max_iters=200):
+def laplace_grid_oracle(model, data, grid_spec=None, *, gtol=1e-6, max_iters=200, mode="reference"):
     """Grid-marginalised evidence over (c_g, sigma_g) with nested Laplace in
     the coefficients (reference evidence.py:330-426).  Nodes run concurrently
-    on the device, each from a = 0 (the reference warm-starts along a
-    serpentine path; the node optimum is the same to the optimiser
-    tolerance); nodes that fail from a = 0 are retried from the last
-    converged node before them in serpentine order (the reference's rule).  Same errors: ValueError for unsuitable models / pinned
-    values or a non-finite starting objective, RuntimeError when more than
-    ``skip_tolerance`` of the nodes fail."""
+    on the device; with the default ``mode="reference"`` each starts from the
+    reference's serpentine a_warm (laplace_grid_nodes), so the set of failed
+    nodes -- and the "untrustworthy" RuntimeError past ``skip_tolerance`` --
+    follows the reference.  Same errors: ValueError for unsuitable models /
+    pinned values or a non-finite starting objective, RuntimeError when more
+    than ``skip_tolerance`` of the nodes fail."""
     grid = GridSpec() if grid_spec is None else grid_spec
-    values, status, _ = laplace_grid_nodes(model, data, grid, gtol=gtol, max_iters=max_iters)
+    values, status, _ = laplace_grid_nodes(model, data, grid, gtol=gtol, max_iters=max_iters, mode=mode)
     if np.any(status == 3):
         raise ValueError("objective is not finite at the starting point")
     skipped = int(np.count_nonzero(status))

@@ -37,13 +37,46 @@ def test_nodes_match_oracle_zero_start(case):
         data, model = logi()
         args = (3.0, 1.0, 3.0, 1.0)
     spec = GridSpec(*args, pinned=(("c_l", 1.0),))
-    v, st, it = laplace_grid_nodes(model, data, spec)
+    v, st, it = laplace_grid_nodes(model, data, spec, mode="robust")  # pass 1 = a = 0 starts
     ov, ost, _ = oracle.laplace_grid_nodes(oracle.OTarget(model, data), *args, (("c_l", 1.0),), warm="zero")
     np.testing.assert_array_equal(st, ost)
     ok = st == 0
     # same algorithm and start; reductions differ in order -> optimiser-tolerance agreement
     assert np.max(np.abs(v[ok] - ov[ok])) < 1e-7
     assert np.all(it[ok] > 0)
+
+
+@pytest.mark.parametrize("case", ["conj", "logi"])
+def test_reference_mode_nodes_match_serpentine_oracle(case):
+    """mode="reference": every node from the reference's serpentine a_warm; the oracle runs the
+    reference's sequential chain (bit-exact with it, tests/test_laplace_oracle.py)."""
+    if case == "conj":
+        data, model = conj()
+        args = (2.0, 0.5, 2.0, 0.5)
+    else:
+        data, model = logi()
+        args = (3.0, 1.0, 3.0, 1.0)
+    v, st, it = laplace_grid_nodes(model, data, GridSpec(*args, pinned=(("c_l", 1.0),)))
+    ov, ost, _ = oracle.laplace_grid_nodes(oracle.OTarget(model, data), *args, (("c_l", 1.0),))
+    np.testing.assert_array_equal(st, ost)
+    ok = st == 0
+    assert np.max(np.abs(v[ok] - ov[ok])) < 1e-6
+
+
+def test_default_grid_fails_like_the_reference():
+    """The paper's grid use (simulated logistic, N = 500, default 400 x 200 GridSpec): the
+    reference's serpentine chain fails 3 678 of 80 000 nodes there and raises "untrustworthy"
+    (CPU restatement, bit-exact with the reference's code path: profiles/r1_laplace_grid.md).
+    mode="reference" reproduces the failure rate and the error; mode="robust" returns a value."""
+    data, _ = rrgp.simulate_logistic(1, n=500, seed=0)
+    model = rrgp.build_model("logistic", data.x)
+    spec = GridSpec(pinned=(("c_l", 1.0),))
+    v, st, _ = laplace_grid_nodes(model, data, spec)
+    failed = int(np.count_nonzero(st))
+    assert 0.8 * 3678 <= failed <= 1.2 * 3678, failed
+    with pytest.raises(RuntimeError, match="untrustworthy"):
+        laplace_grid_oracle(model, data, spec)
+    assert math.isfinite(laplace_grid_oracle(model, data, spec, mode="robust"))
 
 
 def test_grid_evidence_matches_reference():

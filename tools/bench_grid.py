@@ -18,6 +18,7 @@ ap.add_argument("--n", type=int, default=500)
 ap.add_argument("--cpu-nodes", type=int, default=12)
 ap.add_argument("--c-mesh", type=float, default=0.01)
 ap.add_argument("--sigma-mesh", type=float, default=0.02)
+ap.add_argument("--mode", default="reference", choices=["reference", "robust"])
 args = ap.parse_args()
 
 from paper_2511_06407_b200 import rrgp  # noqa: E402
@@ -34,9 +35,9 @@ nc, ns = [c.size for c in spec.centers()]
 # warm-up on a tiny grid (module load, first launch)
 laplace_grid_nodes(model, data, GridSpec(1.0, 0.5, 1.0, 0.5, pinned=(("c_l", 1.0),)))
 t0 = time.perf_counter()
-v, st, it = laplace_grid_nodes(model, data, spec)
+v, st, it = laplace_grid_nodes(model, data, spec, mode=args.mode)
 gpu_s = time.perf_counter() - t0
-print(f"model {args.model} N={args.n}: grid {nc} x {ns} = {nc * ns} nodes on GPU in {gpu_s:.2f} s "
+print(f"mode {args.mode}: model {args.model} N={args.n}: grid {nc} x {ns} = {nc * ns} nodes on GPU in {gpu_s:.2f} s "
       f"({nc * ns / gpu_s:.0f} nodes/s); failed {int(np.count_nonzero(st))}; L-BFGS iterations "
       f"median {int(np.median(it))}, max {int(np.max(it))}")
 
