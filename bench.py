@@ -205,6 +205,69 @@ def run_reference_c4(args):
     print(json.dumps(line), flush=True)
 
 
+_W5 = {}
+
+
+def _c5_init():
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    try:
+        import threadpoolctl
+
+        threadpoolctl.threadpool_limits(1)
+    except Exception:
+        pass
+    import oracle
+
+    models, data = workload_c5()
+    _W5["oracle"] = oracle
+    _W5["targets"] = [(oracle.OTarget(m, data), eps) for m, eps in models]
+
+
+def _c5_worker(args):
+    m, seed, tau, A, C = args
+    oracle = _W5["oracle"]
+    t, eps = _W5["targets"][m]
+    tt = t.at_temperature(tau)
+    cfg = oracle.OConfig(epsilon=eps, leapfrogs=C, moves=A, burnin=0, seed=seed)
+    t0 = time.perf_counter()
+    oracle.run_chain(tt, cfg, tt.initial_point())
+    return A * C, time.perf_counter() - t0
+
+
+def run_reference_c5(args):
+    """--impl reference at C5: the reference's process-pool parallelism (evidence.py:237-239),
+    one (model, chain) unit per host core per step, each unit one rung (cold start + A moves of
+    C leapfrogs); units cycle through the four models."""
+    cores = os.cpu_count() or 1
+    A, C = args.c5_moves, args.leapfrogs or 10
+    pool = mp.get_context("spawn").Pool(cores, initializer=_c5_init)
+    pool.map(_c5_worker, [(k % 4, k, 1.0, 1, 1) for k in range(cores)])
+    for w in range(args.warmup):
+        pool.map(_c5_worker, [(k % 4, 100 + k, 0.5, 1, 1) for k in range(cores)])
+    total, t_all = 0, 0.0
+    for k in range(args.steps):
+        jobs = [((k * cores + j) % 4, 1000 * k + j, 0.5, A, C) for j in range(cores)]
+        t0 = time.perf_counter()
+        out = pool.map(_c5_worker, jobs)
+        t_all += time.perf_counter() - t0
+        total += sum(o[0] for o in out)
+    pool.close()
+    pool.join()
+    value = total / t_all
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "chain-rung-leapfrogs/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_all / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (reference generator simulate_meanvar(2, 19, n=2000, seed=0))",
+        "config": {"workload": C5_NAME, "moves_per_rung": A, "leapfrogs": C, "units_per_step": cores},
+        "cpu_baseline": {"value": value, "unit": "chain-rung-leapfrogs/s", "cores": cores, "kind": "port",
+                         "sample": f"{cores} processes x one rung ({A} moves x {C} leapfrogs + cold start) per step, "
+                                   "models round-robin (oracle port, OPENBLAS_NUM_THREADS=1)"},
+        "e2e": {"value": value, "unit": "chain-rung-leapfrogs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
 def run_reference(args):
     """--impl reference: the reference algorithm on all host cores."""
     rank = int(os.environ.get("RANK", "0"))
@@ -212,6 +275,9 @@ def run_reference(args):
         return
     if args.workload == "c4":
         run_reference_c4(args)
+        return
+    if args.workload == "c5":
+        run_reference_c5(args)
         return
     cores = os.cpu_count() or 1
     # each step: every core runs one chain for `lf` leapfrogs (bounded sample)
@@ -525,6 +591,146 @@ def run_gpu_c4(args):
         dist.destroy_process_group()
 
 
+C5_MODELS = (("l-mean", 1e-4), ("nl-mean", 1e-4), ("l-meanvar", 1e-4), ("nl-meanvar", 8e-5))
+C5_NAME = ("C5 model evidence: l-mean / nl-mean / l-meanvar / nl-meanvar (d = 26/84/47/163) on "
+           "simulate_meanvar(2, 19, n=2000, seed=0), 64 chains each, default_ladder().thin(4) (26 rungs)")
+
+
+def workload_c5():
+    from paper_2511_06407_b200 import rrgp
+
+    data, _ = rrgp.simulate_meanvar(2, 19, n=2000, seed=0)
+    return [(rrgp.build_model(name, data.x), eps) for name, eps in C5_MODELS], data
+
+
+def run_gpu_c5(args):
+    """C5: (model, chain) units u = m*Z + z on rank u mod W; one step = one rung
+    of the ladder walk (cold start at the rung's temperature + A moves of C leapfrogs,
+    evidence.py:142-163) for every local unit, the four models on their own streams."""
+    torch, dist, world, rank, dev_index = _dist_setup()
+    from paper_2511_06407_b200.evidence import default_ladder
+    from paper_2511_06407_b200.posterior import PosteriorTarget
+    from paper_2511_06407_b200.sampler import ChainConfig, DeviceChains
+
+    Z, A, C = args.c5_chains, args.c5_moves, args.leapfrogs or 10
+    ladder = default_ladder(moves_per_rung=A, leapfrogs=C, chains=Z).thin(4)
+    models, data = workload_c5()
+    n_units = len(models) * Z
+    units = [u for u in range(n_units) if u % world == rank]
+    batches = []
+    for m, (model, eps) in enumerate(models):
+        zs = [u % Z for u in units if u // Z == m]
+        if not zs:
+            continue
+        target = PosteriorTarget(model, data)
+        cfg = ChainConfig(epsilon=eps, leapfrogs=C, moves=A, burnin=0, warm_order=args.warm_order or "cyclic")
+        ch = DeviceChains(target.device, np.ones(len(zs)), cfg)
+        ch.set_q(np.tile(target.initial_point(), (len(zs), 1)))
+        batches.append({"m": m, "zs": zs, "ch": ch, "d": target.dim, "stream": torch.cuda.Stream(),
+                        "rng": np.random.default_rng([rank, m])})
+    n_local = sum(len(b["zs"]) for b in batches)
+
+    def draws(b):
+        z = b["rng"].standard_normal((A, len(b["zs"]), b["d"]))
+        with np.errstate(divide="ignore"):
+            lu = np.log(b["rng"].uniform(size=(A, len(b["zs"]))))
+        return z, lu
+
+    n_steps = args.warmup + args.steps
+    for b in batches:
+        b["in"] = [tuple(torch.from_numpy(a).cuda() for a in draws(b)) for _ in range(n_steps)]
+    main = torch.cuda.current_stream()
+
+    def step(k):
+        tau = float(ladder.taus[k % ladder.size])
+        ev0 = torch.cuda.Event()
+        ev0.record(main)
+        ends = []
+        for b in batches:
+            with torch.cuda.stream(b["stream"]):
+                b["stream"].wait_event(ev0)
+                b["ch"].tau.fill_(tau)
+                b["ch"].init()  # the rung's cold start (sampler.py:322-328)
+                b["ch"].run(A, *b["in"][k], move_offset=0)
+                e = torch.cuda.Event()
+                e.record(b["stream"])
+                ends.append(e)
+        for e in ends:
+            main.wait_event(e)
+
+    for w in range(args.warmup):
+        step(w)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    times = []
+    with ClockSampler(dev_index) as clocks:
+        t_wall = time.perf_counter()
+        for k in range(args.steps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(main)
+            step(args.warmup + k)
+            e1.record(main)
+            times.append((e0, e1))
+        torch.cuda.synchronize()
+        t_wall = time.perf_counter() - t_wall
+    bad = sum(int(np.count_nonzero(b["ch"].status_host())) for b in batches)
+    dev_s = sum(a.elapsed_time(b) for a, b in times) / 1e3
+    t_max = torch.tensor([dev_s], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
+    T = float(t_max.item())
+    value = n_units * A * C * args.steps / T
+
+    # e2e through the public API: run_chains per model (host RNG draws in the reference's
+    # order, H2D inside, records and positions back to the host)
+    from paper_2511_06407_b200.sampler import run_chains
+    e2e_steps = max(1, min(args.steps, args.e2e_steps))
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    h2d = d2h = 0
+    for k in range(e2e_steps):
+        tau = float(ladder.taus[k % ladder.size])
+        for b in batches:
+            model, _ = models[b["m"]]
+            tgt = PosteriorTarget(model, data, tau)
+            q0 = b["ch"].q.cpu().numpy()
+            res = run_chains(tgt, b["ch"].config, [1000 * k + z for z in b["zs"]], q0)
+            h2d += len(b["zs"]) * (A * b["d"] + A + b["d"]) * 8
+            d2h += len(b["zs"]) * (A * 7 + b["d"]) * 8
+    torch.cuda.synchronize()
+    e2e_t = time.perf_counter() - t0
+    e2e_max = torch.tensor([e2e_t], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(e2e_max, op=dist.ReduceOp.MAX)
+    e2e_value = n_units * A * C * e2e_steps / float(e2e_max.item())
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "chain-rung-leapfrogs/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * T / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (reference generator simulate_meanvar(2, 19, n=2000, seed=0))",
+            "config": {"workload": C5_NAME, "units": n_units, "units_on_rank0": n_local,
+                       "moves_per_rung": A, "leapfrogs": C,
+                       "step": "one ladder rung (cold start + A moves) of every (model, chain) unit",
+                       "parallelism": f"(model, chain) units sharded over {world} rank(s), unit u on rank u mod W",
+                       "warm_order": batches[0]["ch"].config.warm_order if batches else None,
+                       "status_nonzero": bad},
+            "gpu_launches": args.steps * 2 * len(batches),
+            "e2e": {"value": e2e_value, "unit": "chain-rung-leapfrogs/s", "h2d_bytes_per_step": h2d // e2e_steps,
+                    "d2h_bytes_per_step": d2h // e2e_steps, "steps": e2e_steps},
+            "roofline": None,
+            "roofline_note": "latency-bound (SURVEY.md 8(d): neither roofline binds at d <= 163)",
+            "clocks": clocks.summary(), "wall_s_timed": t_wall,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def model_rows(data):
     return int(np.asarray(data.y).shape[0])
 
@@ -721,7 +927,9 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c4", choices=["c4", "c2"])
+    ap.add_argument("--workload", default="c4", choices=["c4", "c2", "c5"])
+    ap.add_argument("--c5-chains", type=int, default=64)
+    ap.add_argument("--c5-moves", type=int, default=2, help="moves per rung (C5)")
     ap.add_argument("--leapfrogs", type=int, default=0, help="leapfrogs per move (C4 default 100)")
     ap.add_argument("--e2e-steps", type=int, default=3, help="moves timed end to end (C4)")
     ap.add_argument("--chains", type=int, default=0, help="chains per GPU (default SMs x chains-per-sm)")
@@ -738,6 +946,8 @@ def main():
         run_reference(args)
     elif args.workload == "c4":
         run_gpu_c4(args)
+    elif args.workload == "c5":
+        run_gpu_c5(args)
     else:
         args.warm_order = args.warm_order or "cyclic"
         run_gpu(args)

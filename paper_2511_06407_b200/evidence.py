@@ -7,10 +7,11 @@ What changes is how chains execute:
 
 * all chains of a rank advance together: per rung one cold-start launch and
   one on-device move-loop launch for the whole batch (one CTA per chain);
-* chains are sharded across ranks (chain z on rank z mod W) when
+* (model, chain) units are sharded across ranks (unit u on rank u mod W;
+  ``evidence_sweep`` for several models, ``thermo_integrate`` for one) when
   ``torch.distributed`` is initialised; rungs are never split (SURVEY.md M4);
 * the only collective is one all-gather of the per-chain rung values
-  (NCCL on GPU ranks, gloo in CPU tests), after the ladder.
+  (NCCL on GPU ranks, gloo in CPU tests), after the ladders.
 
 Chain results depend only on (seed, z), so estimates are bitwise identical
 for any world size.
@@ -241,41 +242,9 @@ def gather_chain_values(local_ids, local_values, n_chains, n_rungs, local_errors
     return (full, errors) if return_errors else full
 
 
-def thermo_integrate(model, data, ladder, config, *, rung_average=False, warmup_segment_moves=50,
-                     warmup_max_segments=8, warmup_pvalue=0.05, spread_moves=10, initial=None,
-                     threads=1, progress=None, target=None, ladder_runner=None,
-                     warmup_runner=None):
-    """Estimate ln P(X) by thermodynamic integration (evidence.py:184-274).
-
-    ``threads`` is accepted for API compatibility; chains run as one device
-    batch per rank instead of a process pool.  ``ladder_runner`` /
-    ``warmup_runner`` substitute the chain executors (tests inject the CPU
-    oracle to exercise the multi-rank logic without a GPU).
-    """
-    if ladder_runner is None:
-        if not hasattr(config, "epsilon") or not hasattr(config, "leapfrogs"):
-            raise TypeError("config must be a ChainConfig")
-        config = as_chain_config(config)
-    seed_root = config.seed if isinstance(config.seed, np.random.SeedSequence) \
-        else np.random.SeedSequence(config.seed)
-    n_chains = ladder.chains
-    seqs = seed_root.spawn(warmup_max_segments + n_chains)
-    if target is None:
-        target = PosteriorTarget(model, data)
-    warnings: list = []
-    q_warm = warm_up(target, config, seqs[:warmup_max_segments], warmup_segment_moves, warmup_pvalue,
-                     warnings, initial, runner=warmup_runner or run_chain)
-    _, rank, world = _dist_info()
-    mine = [z for z in range(n_chains) if z % world == rank]
-    runner = ladder_runner or device_ladder_runner
-    vals, errs = runner(target, [seqs[warmup_max_segments + z] for z in mine], q_warm, ladder, config,
-                        rung_average, spread_moves)
-    # failed chains travel as an all-NaN row plus their error code (the reference maps them
-    # to NaN and keeps the ChainError text in the warning, evidence.py:248-253)
-    rung_values, chain_errors = gather_chain_values(mine, vals, n_chains, ladder.size, errs,
-                                                    return_errors=True)
-    if progress is not None:
-        progress(f"evidence: {n_chains} chains finished on {world} rank(s)")
+def _aggregate(rung_values, chain_errors, ladder, warnings):
+    """Per-chain trapezoid, cross-chain mean and stderr, rung means (evidence.py:246-274)."""
+    n_chains = rung_values.shape[0]
     per_chain = []
     for z in range(n_chains):
         row = rung_values[z]
@@ -300,7 +269,82 @@ def thermo_integrate(model, data, ladder, config, *, rung_average=False, warmup_
                             warnings=warnings, rung_values=rung_values)
 
 
-__all__ = ["TemperLadder", "default_ladder", "ti_variance", "EvidenceEstimate", "thermo_integrate",
+def evidence_sweep(models, data, ladder, config, *, rung_average=False, warmup_segment_moves=50,
+                   warmup_max_segments=8, warmup_pvalue=0.05, spread_moves=10, initial=None, progress=None,
+                   targets=None, ladder_runner=None, warmup_runner=None):
+    """Thermodynamic integration for several competing models at once (the paper's model
+    comparison), sharded over ``torch.distributed`` ranks by unit.
+
+    The independent units are (model m, chain z) pairs, u = m * Z + z, placed on rank
+    u mod W; rungs are never split.  Each model is seeded exactly as
+    ``thermo_integrate(models[m], ...)`` with the same config, so every estimate equals the
+    single-model, single-process one bit for bit at any world size.  Every rank recomputes
+    the (deterministic) warm-up of every model; the only collective is one
+    ``all_gather_into_tensor`` of [ceil(U/W), S+2] fp64 after the ladders (unit id, error
+    code, rung values), NCCL on GPU ranks and gloo on CPU.  Returns one EvidenceEstimate per
+    model.  ``targets`` (one per model), ``ladder_runner`` and ``warmup_runner`` substitute
+    the targets and chain executors (tests inject the CPU oracle)."""
+    if ladder_runner is None:
+        if not hasattr(config, "epsilon") or not hasattr(config, "leapfrogs"):
+            raise TypeError("config must be a ChainConfig")
+        config = as_chain_config(config)
+    n_models = len(models)
+    Z, S = ladder.chains, ladder.size
+    _, rank, world = _dist_info()
+    units = [u for u in range(n_models * Z) if u % world == rank]
+    by_model = {}
+    for u in units:
+        by_model.setdefault(u // Z, []).append(u % Z)
+    warn = [[] for _ in range(n_models)]
+    local_vals, local_errs = {}, {}
+    for m in range(n_models):
+        # every rank runs every model's warm-up (deterministic from the seed), so the warm-up
+        # warnings agree everywhere without a second collective
+        seed_root = config.seed if isinstance(config.seed, np.random.SeedSequence) \
+            else np.random.SeedSequence(config.seed)
+        seqs = seed_root.spawn(warmup_max_segments + Z)
+        target = targets[m] if targets is not None else PosteriorTarget(models[m], data)
+        q_warm = warm_up(target, config, seqs[:warmup_max_segments], warmup_segment_moves, warmup_pvalue,
+                         warn[m], initial, runner=warmup_runner or run_chain)
+        zs = by_model.get(m, [])
+        if not zs:
+            continue
+        runner = ladder_runner or device_ladder_runner
+        vals, errs = runner(target, [seqs[warmup_max_segments + z] for z in zs], q_warm, ladder, config,
+                            rung_average, spread_moves)
+        for k, z in enumerate(zs):
+            local_vals[m * Z + z] = vals[k]
+            local_errs[m * Z + z] = errs[k]
+    ids = sorted(local_vals)
+    allv, alle = gather_chain_values(ids, [local_vals[u] for u in ids], n_models * Z, S,
+                                     [local_errs[u] for u in ids], return_errors=True)
+    if progress is not None:
+        progress(f"evidence: {n_models} model(s) x {Z} chains finished on {world} rank(s)")
+    out = []
+    for m in range(n_models):
+        out.append(_aggregate(allv[m * Z:(m + 1) * Z], alle[m * Z:(m + 1) * Z], ladder, warn[m]))
+    return out
+
+
+def thermo_integrate(model, data, ladder, config, *, rung_average=False, warmup_segment_moves=50,
+                     warmup_max_segments=8, warmup_pvalue=0.05, spread_moves=10, initial=None,
+                     threads=1, progress=None, target=None, ladder_runner=None,
+                     warmup_runner=None):
+    """Estimate ln P(X) by thermodynamic integration (evidence.py:184-274).
+
+    ``threads`` is accepted for API compatibility; chains run as one device
+    batch per rank instead of a process pool.  ``ladder_runner`` /
+    ``warmup_runner`` substitute the chain executors (tests inject the CPU
+    oracle to exercise the multi-rank logic without a GPU).
+    """
+    return evidence_sweep([model], data, ladder, config, rung_average=rung_average,
+                          warmup_segment_moves=warmup_segment_moves, warmup_max_segments=warmup_max_segments,
+                          warmup_pvalue=warmup_pvalue, spread_moves=spread_moves, initial=initial,
+                          progress=progress, targets=None if target is None else [target],
+                          ladder_runner=ladder_runner, warmup_runner=warmup_runner)[0]
+
+
+__all__ = ["TemperLadder", "default_ladder", "ti_variance", "EvidenceEstimate", "thermo_integrate", "evidence_sweep",
            "gather_chain_values", "device_ladder_runner", "warm_up", "JacobiError"]
 
 

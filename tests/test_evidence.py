@@ -154,3 +154,73 @@ def test_device_thermo_integrate_matches_reference_golden():
     assert rel_err(est.rung_values, g["rung_values"]) < 1e-9
     assert rel_err(est.per_chain, g["per_chain"]) < 1e-9
     assert est.bme_mean == pytest.approx(float(g["bme_mean"]), rel=1e-9)
+
+
+# -- several models, (model, chain) units sharded over ranks --------------
+
+
+def _two_models():
+    g, model, data = case("ti_small")
+    from paper_2511_06407_b200 import rrgp
+    other = rrgp.build_model("logistic", data.x, feature_count=6)
+    ladder = E.TemperLadder(taus=g["taus"], moves_per_rung=3, leapfrogs=5, chains=3)
+    cfg = ChainConfig(epsilon=0.02, leapfrogs=5, moves=10, burnin=0, seed=123)
+    return [model, other], data, ladder, cfg
+
+
+def _sweep(models, data, ladder, cfg):
+    return E.evidence_sweep(models, data, ladder, cfg, warmup_segment_moves=10, warmup_max_segments=2,
+                            spread_moves=2, targets=[oracle.OTarget(m, data) for m in models],
+                            ladder_runner=oracle_ladder_runner, warmup_runner=oracle_warmup_runner)
+
+
+def test_sweep_equals_per_model_thermo_integrate():
+    models, data, ladder, cfg = _two_models()
+    ests = _sweep(models, data, ladder, cfg)
+    for m, est in zip(models, ests):
+        one = E.thermo_integrate(m, data, ladder, cfg, warmup_segment_moves=10, warmup_max_segments=2,
+                                 spread_moves=2, target=oracle.OTarget(m, data),
+                                 ladder_runner=oracle_ladder_runner, warmup_runner=oracle_warmup_runner)
+        np.testing.assert_array_equal(est.rung_values, one.rung_values)
+        assert est.bme_mean == one.bme_mean and est.bme_stderr == one.bme_stderr
+
+
+def _sweep_rank_main(rank, world, port, out_dir):
+    import torch.distributed as dist
+
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    try:
+        models, data, ladder, cfg = _two_models()
+        ests = _sweep(models, data, ladder, cfg)
+        from paper_2511_06407_b200.diagnostics import distributed_split_rhat
+        chains = np.random.default_rng(5).standard_normal((7, 40, 3))
+        mine = [z for z in range(7) if z % world == rank]
+        rh = distributed_split_rhat(chains[mine], mine, 7)
+        with open(os.path.join(out_dir, f"rank{rank}.pkl"), "wb") as fh:
+            pickle.dump(([e.rung_values for e in ests], [e.bme_mean for e in ests], rh), fh)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_unit_sharding_is_bitwise_identical(world):
+    """Several models' (model, chain) units over W gloo ranks, one all-gather == one process,
+    bit for bit; the replica split-R-hat gathered from per-chain summaries == split_rhat."""
+    import torch.multiprocessing as tmp
+
+    from paper_2511_06407_b200.diagnostics import split_rhat
+
+    models, data, ladder, cfg = _two_models()
+    ref = _sweep(models, data, ladder, cfg)
+    ref_rh = split_rhat(np.random.default_rng(5).standard_normal((7, 40, 3)))
+    port = _free_port()
+    with tempfile.TemporaryDirectory() as d:
+        tmp.spawn(_sweep_rank_main, args=(world, port, d), nprocs=world, join=True)
+        for rank in range(world):
+            with open(os.path.join(d, f"rank{rank}.pkl"), "rb") as fh:
+                rvs, bmes, rh = pickle.load(fh)
+            for k in range(len(models)):
+                np.testing.assert_array_equal(rvs[k], ref[k].rung_values)
+                assert bmes[k] == ref[k].bme_mean
+            np.testing.assert_array_equal(rh, ref_rh)
