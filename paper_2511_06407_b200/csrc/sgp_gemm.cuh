@@ -17,11 +17,25 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
-#define GM_BM 64
-#define GM_BN 64
 #define GM_BK 32
-#define GM_THREADS 128
-#define GM_STAGES 3
+
+// CTA tile configurations.  Big: 128 x 64 tile, 2 x 2 warps of 64 x 32 (8 x 4 DMMA fragments,
+// 64 accumulator doubles per thread), 2 stages -- more independent DMMAs per warp and half
+// the operand traffic per flop (+16 % on d^3 at d = 2083, measured with tools/gemm_bench.cu).
+// Small: 64 x 64, 2 x 2 warps of 32 x 32, 3 stages, for outputs with too few big tiles to
+// fill the GPU (the 1040 x 1040 Hessian blocks, the block-Jacobi 64 x 64 updates).
+struct GmSmall {
+    static constexpr int BM = 64, BN = 64, WARPS_M = 2, WARPS_N = 2, STAGES = 3;
+};
+struct GmBig {
+    static constexpr int BM = 128, BN = 64, WARPS_M = 2, WARPS_N = 2, STAGES = 2;
+};
+template <class CFG>
+struct GmGeo {
+    static constexpr int THREADS = 32 * CFG::WARPS_M * CFG::WARPS_N;
+    static constexpr int FI = CFG::BM / (8 * CFG::WARPS_M), FJ = CFG::BN / (8 * CFG::WARPS_N);
+};
+#define GM_THREADS_MAX 128
 
 struct GemmArgs {
     int M, N, K;
@@ -63,19 +77,20 @@ __device__ __forceinline__ void gm_cp8(void *dst, const void *src, bool valid) {
 
 // shared tile geometry: "row" = the contiguous global dimension
 // A: TA ? [BK][BM] : [BM][BK];  B: TB ? [BN][BK] : [BK][BN]
-template <int TA, int TB>
+template <int TA, int TB, class CFG>
 struct GmTile {
-    static constexpr int A_ROWS = TA ? GM_BK : GM_BM, A_COLS = TA ? GM_BM : GM_BK;
-    static constexpr int B_ROWS = TB ? GM_BN : GM_BK, B_COLS = TB ? GM_BK : GM_BN;
+    static constexpr int A_ROWS = TA ? GM_BK : CFG::BM, A_COLS = TA ? CFG::BM : GM_BK;
+    static constexpr int B_ROWS = TB ? CFG::BN : GM_BK, B_COLS = TB ? GM_BK : CFG::BN;
     static constexpr int A_LD = A_COLS + 4, B_LD = B_COLS + 4;
     static constexpr int A_SZ = A_ROWS * A_LD, B_SZ = B_ROWS * B_LD;
     static constexpr int STAGE = A_SZ + B_SZ + GM_BK;  // + per-k scale
-    static constexpr size_t SMEM = (size_t)GM_STAGES * STAGE * sizeof(double);
+    static constexpr size_t SMEM = (size_t)CFG::STAGES * STAGE * sizeof(double);
 };
 
-template <int TA, int TB>
+template <int TA, int TB, class CFG>
 __device__ __forceinline__ void gm_issue(const GemmArgs &g, double *st, int m0, int n0, int k0) {
-    using T = GmTile<TA, TB>;
+    using T = GmTile<TA, TB, CFG>;
+    constexpr int GM_THREADS = GmGeo<CFG>::THREADS, GM_BM = CFG::BM, GM_BN = CFG::BN;
     const int tid = threadIdx.x;
     double *As = st, *Bs = st + T::A_SZ, *Ss = st + T::A_SZ + T::B_SZ;
     // operand bases and k offsets of this k-tile (K-split gather)
@@ -84,7 +99,21 @@ __device__ __forceinline__ void gm_issue(const GemmArgs &g, double *st, int m0, 
     const int dka = sa ? -g.ksplit : 0, dkb = sb ? -g.ksplit : 0;
     // A: rows of A_COLS doubles, A_COLS/2 16-byte chunks per row
     constexpr int ACH = T::A_COLS / 2, BCH = T::B_COLS / 2;
-    if (!g.a16) {
+    // interior tiles (no edge, no K-split switch inside the tile): one base pointer, no
+    // per-copy bounds tests -- the index arithmetic of the general path dominated the
+    // issue slots of the main loop
+    const bool a_in = g.a16 && !sa && !(g.A2 && g.ksplit && k0 + GM_BK > g.ksplit) && m0 + GM_BM <= g.M &&
+                      k0 + GM_BK <= g.K;
+    const bool b_in = g.b16 && !sb && !(g.B2 && g.ksplit && k0 + GM_BK > g.ksplit) && n0 + GM_BN <= g.N &&
+                      k0 + GM_BK <= g.K;
+    if (a_in) {
+        const double *base = Ab + (size_t)(TA ? k0 : m0) * g.lda + (TA ? m0 : k0);
+#pragma unroll
+        for (int e = tid; e < T::A_ROWS * ACH; e += GM_THREADS) {
+            const int r = e / ACH, c = (e - r * ACH) * 2;
+            gm_cp16(As + r * T::A_LD + c, base + (size_t)r * g.lda + c, true);
+        }
+    } else if (!g.a16) {
         for (int e = tid; e < T::A_ROWS * T::A_COLS; e += GM_THREADS) {
             const int r = e / T::A_COLS, c = e - r * T::A_COLS;
             const int gr = (TA ? k0 : m0) + r, gc = (TA ? m0 : k0) + c;
@@ -110,7 +139,14 @@ __device__ __forceinline__ void gm_issue(const GemmArgs &g, double *st, int m0, 
         }
     }
     }
-    if (!g.b16) {
+    if (b_in) {
+        const double *base = Bb + (size_t)(TB ? n0 : k0) * g.ldb + (TB ? k0 : n0);
+#pragma unroll
+        for (int e = tid; e < T::B_ROWS * BCH; e += GM_THREADS) {
+            const int r = e / BCH, c = (e - r * BCH) * 2;
+            gm_cp16(Bs + r * T::B_LD + c, base + (size_t)r * g.ldb + c, true);
+        }
+    } else if (!g.b16) {
         for (int e = tid; e < T::B_ROWS * T::B_COLS; e += GM_THREADS) {
             const int r = e / T::B_COLS, c = e - r * T::B_COLS;
             const int gr = (TB ? n0 : k0) + r, gc = (TB ? k0 : n0) + c;
@@ -147,28 +183,32 @@ __device__ __forceinline__ void gm_issue(const GemmArgs &g, double *st, int m0, 
     asm volatile("cp.async.commit_group;\n" ::);
 }
 
-template <int TA, int TB>
+template <int TA, int TB, class CFG>
 __device__ __forceinline__ void gm_body(const GemmArgs &g) {
-    using T = GmTile<TA, TB>;
+    using T = GmTile<TA, TB, CFG>;
+    constexpr int GM_BM = CFG::BM, GM_BN = CFG::BN, GM_STAGES = CFG::STAGES;
+    constexpr int GM_WARPS_N = CFG::WARPS_N, GM_WARPS_M = CFG::WARPS_M;
+    constexpr int GM_FI = GmGeo<CFG>::FI, GM_FJ = GmGeo<CFG>::FJ;
     const int tm = blockIdx.y, tn = blockIdx.x;
-    if (g.upper_only && tm > tn) return;
+    // symmetric outputs: skip tiles entirely below the diagonal (mirrored afterwards)
+    if (g.upper_only && tm * GM_BM > tn * GM_BN + GM_BN - 1) return;
     if (tm * GM_BM >= g.M || tn * GM_BN >= g.N) return;  // batched launches size the grid for the largest
     extern __shared__ __align__(16) double gsm[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+    const int wm = (warp / GM_WARPS_N) * (GM_BM / GM_WARPS_M), wn = (warp % GM_WARPS_N) * (GM_BN / GM_WARPS_N);
     const int gid = lane >> 2, tig = lane & 3;
     const int m0 = tm * GM_BM, n0 = tn * GM_BN;
     const bool has_scale = g.scale != nullptr;
-    double acc[4][4][2];
+    double acc[GM_FI][GM_FJ][2];
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < GM_FI; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+        for (int j = 0; j < GM_FJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
     const int nk = (g.K + GM_BK - 1) / GM_BK;
 #pragma unroll
     for (int s = 0; s < GM_STAGES - 1; ++s) {
         if (s < nk)
-            gm_issue<TA, TB>(g, gsm + s * T::STAGE, m0, n0, s * GM_BK);
+            gm_issue<TA, TB, CFG>(g, gsm + s * T::STAGE, m0, n0, s * GM_BK);
         else
             asm volatile("cp.async.commit_group;\n" ::);
     }
@@ -177,7 +217,7 @@ __device__ __forceinline__ void gm_body(const GemmArgs &g) {
         __syncthreads();
         const int nxt = kt + GM_STAGES - 1;
         if (nxt < nk)
-            gm_issue<TA, TB>(g, gsm + (nxt % GM_STAGES) * T::STAGE, m0, n0, nxt * GM_BK);
+            gm_issue<TA, TB, CFG>(g, gsm + (nxt % GM_STAGES) * T::STAGE, m0, n0, nxt * GM_BK);
         else
             asm volatile("cp.async.commit_group;\n" ::);
         const double *As = gsm + (kt % GM_STAGES) * T::STAGE;
@@ -185,32 +225,36 @@ __device__ __forceinline__ void gm_body(const GemmArgs &g) {
 #pragma unroll
         for (int k4 = 0; k4 < GM_BK; k4 += 4) {
             const int kk = k4 + tig;
-            double af[4], bf[4];
-            const double sk = has_scale ? Ss[kk] : 1.0;
+            double af[GM_FI], bf[GM_FJ];
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
+            for (int i = 0; i < GM_FI; ++i) {
                 const int mm = wm + i * 8 + gid;
-                af[i] = (TA ? As[kk * T::A_LD + mm] : As[mm * T::A_LD + kk]) * sk;
+                af[i] = TA ? As[kk * T::A_LD + mm] : As[mm * T::A_LD + kk];
+            }
+            if (has_scale) {
+                const double sk = Ss[kk];
+#pragma unroll
+                for (int i = 0; i < GM_FI; ++i) af[i] *= sk;
             }
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
+            for (int j = 0; j < GM_FJ; ++j) {
                 const int nn = wn + j * 8 + gid;
                 bf[j] = TB ? Bs[nn * T::B_LD + kk] : Bs[kk * T::B_LD + nn];
             }
 #pragma unroll
-            for (int i = 0; i < 4; ++i)
+            for (int i = 0; i < GM_FI; ++i)
 #pragma unroll
-                for (int j = 0; j < 4; ++j) dmma_m8n8k4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+                for (int j = 0; j < GM_FJ; ++j) dmma_m8n8k4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
         }
     }
     asm volatile("cp.async.wait_group 0;\n" ::);
     // epilogue: C fragment (row gid, cols 2*tig, 2*tig+1)
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < GM_FI; ++i) {
         const int m = m0 + wm + i * 8 + gid;
         if (m >= g.M) continue;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
+        for (int j = 0; j < GM_FJ; ++j) {
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
                 const int n = n0 + wn + j * 8 + 2 * tig + h;
@@ -230,16 +274,16 @@ __device__ __forceinline__ void gm_body(const GemmArgs &g) {
     }
 }
 
-template <int TA, int TB>
-__global__ void __launch_bounds__(GM_THREADS) k_gemm_dmma(GemmArgs g) {
-    gm_body<TA, TB>(g);
+template <int TA, int TB, class CFG>
+__global__ void __launch_bounds__(GM_THREADS_MAX) k_gemm_dmma(GemmArgs g) {
+    gm_body<TA, TB, CFG>(g);
 }
 
 // one GEMM per blockIdx.z (independent outputs); grid sized for the largest
 template <int TA, int TB>
-__global__ void __launch_bounds__(GM_THREADS) k_gemm_dmma_batched(const GemmArgs *gs) {
+__global__ void __launch_bounds__(GM_THREADS_MAX) k_gemm_dmma_batched(const GemmArgs *gs) {
     const GemmArgs g = gs[blockIdx.z];
-    gm_body<TA, TB>(g);
+    gm_body<TA, TB, GmSmall>(g);
 }
 
 // mirror the upper triangle of an n x n matrix into the lower one
@@ -251,34 +295,53 @@ __global__ void k_mirror_upper(double *C, int n, int ldc) {
     }
 }
 
-template <int TA, int TB>
+template <int TA, int TB, class CFG>
 static inline cudaError_t gemm_launch_t(const GemmArgs &g, cudaStream_t s) {
-    using T = GmTile<TA, TB>;
+    using T = GmTile<TA, TB, CFG>;
     static bool configured = false;
     if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(k_gemm_dmma<TA, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaError_t e = cudaFuncSetAttribute(k_gemm_dmma<TA, TB, CFG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)T::SMEM);
         if (e != cudaSuccess) return e;
         configured = true;
     }
-    dim3 grid((g.N + GM_BN - 1) / GM_BN, (g.M + GM_BM - 1) / GM_BM);
-    k_gemm_dmma<TA, TB><<<grid, GM_THREADS, T::SMEM, s>>>(g);
+    dim3 grid((g.N + CFG::BN - 1) / CFG::BN, (g.M + CFG::BM - 1) / CFG::BM);
+    k_gemm_dmma<TA, TB, CFG><<<grid, GmGeo<CFG>::THREADS, T::SMEM, s>>>(g);
     return cudaGetLastError();
 }
+
+// Tiles a launch computes (upper_only skips those entirely below the diagonal).
+template <class CFG>
+static inline long gemm_tiles(const GemmArgs &g) {
+    const int tm = (g.M + CFG::BM - 1) / CFG::BM, tn = (g.N + CFG::BN - 1) / CFG::BN;
+    if (!g.upper_only) return (long)tm * tn;
+    long n = 0;
+    for (int i = 0; i < tm; ++i)
+        for (int j = 0; j < tn; ++j) n += (i * CFG::BM <= j * CFG::BN + CFG::BN - 1);
+    return n;
+}
+// Big tiles when they fill at least ~0.85 of a wave of two CTAs per SM on 148 SMs (measured:
+// d^3 at d = 2083 28.8 vs 25.1 TF/s; the 1040 x 1040 Hessian blocks, 153 big tiles, stay small).
+static inline bool gemm_big_tiles(const GemmArgs &g) { return gemm_tiles<GmBig>(g) >= 250; }
 
 static inline cudaError_t gemm_launch(GemmArgs g, cudaStream_t s) {
     g.a16 = (g.lda % 2 == 0) && ((reinterpret_cast<uintptr_t>(g.A) & 15) == 0);
     g.b16 = (g.ldb % 2 == 0) && ((reinterpret_cast<uintptr_t>(g.B) & 15) == 0);
-    if (g.TA)
-        return g.TB ? gemm_launch_t<1, 1>(g, s) : gemm_launch_t<1, 0>(g, s);
-    return g.TB ? gemm_launch_t<0, 1>(g, s) : gemm_launch_t<0, 0>(g, s);
+    const bool big = gemm_big_tiles(g) && !g.ksplit && !g.C2;
+    if (g.TA) {
+        if (g.TB) return big ? gemm_launch_t<1, 1, GmBig>(g, s) : gemm_launch_t<1, 1, GmSmall>(g, s);
+        return big ? gemm_launch_t<1, 0, GmBig>(g, s) : gemm_launch_t<1, 0, GmSmall>(g, s);
+    }
+    if (g.TB) return big ? gemm_launch_t<0, 1, GmBig>(g, s) : gemm_launch_t<0, 1, GmSmall>(g, s);
+    return big ? gemm_launch_t<0, 0, GmBig>(g, s) : gemm_launch_t<0, 0, GmSmall>(g, s);
 }
 
 // Batched launch: nb descriptors in device memory (all with the same TA, TB
 // and alignment flags, set by the caller); grid covers max M x max N.
 template <int TA, int TB>
 static inline cudaError_t gemm_launch_batched(const GemmArgs *d_gs, int nb, int maxM, int maxN, cudaStream_t s) {
-    using T = GmTile<TA, TB>;
+    using T = GmTile<TA, TB, GmSmall>;
+    constexpr int GM_BM = GmSmall::BM, GM_BN = GmSmall::BN, GM_THREADS = GmGeo<GmSmall>::THREADS;
     static bool configured = false;
     if (!configured) {
         cudaError_t e = cudaFuncSetAttribute(k_gemm_dmma_batched<TA, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize,

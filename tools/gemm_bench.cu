@@ -52,6 +52,33 @@ int main() {
                 fails += err > 1e-12;
                 cudaFree(dA); cudaFree(dB); cudaFree(dC); if (dS) cudaFree(dS);
             }
+    for (int up = 0; up < 2; ++up)  // shapes large enough for the 128 x 64 tiles (gemm_big_tiles)
+        for (int ta = 0; ta < 2; ++ta) {
+            const int M = up ? 2400 : 3000, N = up ? 2400 : 1200, K = 40;
+            GemmArgs g{};
+            g.M = M; g.N = N; g.K = K; g.TA = ta; g.TB = 0; g.upper_only = up;
+            g.lda = ta ? M : K; g.ldb = N; g.ldc = N; g.alpha = 1;
+            std::vector<double> A((size_t)(ta ? K : M) * g.lda), B((size_t)K * N), C((size_t)M * N, 0.0),
+                R((size_t)M * N), S;
+            for (auto &v : A) v = rand() / (double)RAND_MAX - 0.5;
+            for (auto &v : B) v = rand() / (double)RAND_MAX - 0.5;
+            double *dA, *dB, *dC;
+            cudaMalloc(&dA, A.size() * 8); cudaMalloc(&dB, B.size() * 8); cudaMalloc(&dC, C.size() * 8);
+            cudaMemcpy(dA, A.data(), A.size() * 8, cudaMemcpyHostToDevice);
+            cudaMemcpy(dB, B.data(), B.size() * 8, cudaMemcpyHostToDevice);
+            cudaMemset(dC, 0, C.size() * 8);
+            g.A = dA; g.B = dB; g.C = dC;
+            const bool big = gemm_big_tiles(g);
+            gemm_launch(g, 0);
+            cudaMemcpy(C.data(), dC, C.size() * 8, cudaMemcpyDeviceToHost);
+            ref(g, A, B, S, R);
+            double err = 0;
+            for (int m = 0; m < M; ++m)
+                for (int n = up ? m : 0; n < N; ++n) err = fmax(err, fabs(C[(size_t)m * N + n] - R[(size_t)m * N + n]));
+            printf("big-tile case TA=%d upper=%d (big=%d) max err %.3e\n", ta, up, (int)big, err);
+            fails += err > 1e-12 || !big;
+            cudaFree(dA); cudaFree(dB); cudaFree(dC);
+        }
     {   // odd leading dimensions (d = 2083-style buffers) use 8-byte copies
         int M = 37, N = 29, K = 41;
         GemmArgs g{};
