@@ -31,6 +31,7 @@ struct LgPtrs {
     double *bjU, *bjLam, *bjPart;
     int *bjCnt;
     GemmArgs *bjDesc;            // [round][col A | row A | col V even | col V odd][2 * pairs]
+    GemmArgs *hdesc;             // the likelihood-Hessian blocks' batched GEMM descriptors (3)
     // host handles owned by this workspace (one per model, like the buffers above): the
     // high-priority stream of the block-Jacobi A chain and the events ordering it against
     // the caller's stream (in, solved, chain, V update of even / odd rounds)
@@ -1001,13 +1002,37 @@ static int lg_state(LgCtx &c, int qv, int what) {
         k_lg_zero<<<lg_blocks((size_t)d * d), 256, 0, c.s>>>(c.L.H, (size_t)d * d);
         if (c.tau != 0.0 && mp.lik != SGP_LIK_QUADRATIC) {
             const int fields[3] = {F_D2_00, F_D2_01, F_D2_11};
+            // the J(J+1)/2 likelihood blocks in one batched launch (each 1040 x 1040 block alone
+            // fills about half a wave of the GPU at C4)
+            GemmArgs hd[3];
+            int nbk = 0, maxM = 0, maxN = 0;
             for (int j1 = 0; j1 < mp.J; ++j1)
                 for (int j2 = j1; j2 < mp.J; ++j2) {
-                    const double *a = c.L.M.phis + (j1 ? mp.Dp0 : 0);
-                    const double *b = c.L.M.phis + (j2 ? mp.Dp0 : 0);
-                    double *C = c.L.H + (size_t)mp.fstart[j1] * d + mp.fstart[j2];
-                    const double *w = c.L.S + (size_t)fields[j1 + j2] * mp.ld;
-                    lg_gemm(c, mp.D[j1], mp.D[j2], mp.N, a, mp.Dp, 1, b, mp.Dp, 0, w, C, d, c.tau, j1 == j2);
+                    GemmArgs &g = hd[nbk++];
+                    g = GemmArgs{};
+                    g.M = mp.D[j1];
+                    g.N = mp.D[j2];
+                    g.K = mp.N;
+                    g.A = c.L.M.phis + (j1 ? mp.Dp0 : 0);
+                    g.lda = mp.Dp;
+                    g.TA = 1;
+                    g.B = c.L.M.phis + (j2 ? mp.Dp0 : 0);
+                    g.ldb = mp.Dp;
+                    g.scale = c.L.S + (size_t)fields[j1 + j2] * mp.ld;
+                    g.C = c.L.H + (size_t)mp.fstart[j1] * d + mp.fstart[j2];
+                    g.ldc = d;
+                    g.alpha = c.tau;
+                    g.upper_only = j1 == j2;
+                    g.a16 = (g.lda % 2 == 0) && ((reinterpret_cast<uintptr_t>(g.A) & 15) == 0);
+                    g.b16 = (g.ldb % 2 == 0) && ((reinterpret_cast<uintptr_t>(g.B) & 15) == 0);
+                    maxM = std::max(maxM, g.M);
+                    maxN = std::max(maxN, g.N);
+                }
+            // all blocks share TA/TB; the alignment flags agree (same Phi buffer, same ld)
+            cudaMemcpyAsync(c.L.hdesc, hd, sizeof(GemmArgs) * nbk, cudaMemcpyHostToDevice, c.s);
+            gemm_launch_batched<1, 0>(c.L.hdesc, nbk, maxM, maxN, c.s);
+            for (int j1 = 0; j1 < mp.J; ++j1)
+                for (int j2 = j1; j2 < mp.J; ++j2) {
                     if (j1 == j2)
                         k_lg_mirror_block<<<lg_blocks((size_t)mp.D[j1] * mp.D[j1]), 256, 0, c.s>>>(
                             c.L.H, d, mp.fstart[j1], mp.D[j1]);
@@ -1688,6 +1713,7 @@ static int lg_alloc(const ModelDev &M, LgPtrs &L, void **owner) {
                  obC = take((size_t)bnp);
     const size_t ndesc = (size_t)(nbk - 1) * 4 * bnp;
     const size_t obD = take((ndesc * sizeof(GemmArgs) + sizeof(double) - 1) / sizeof(double) + 2);
+    const size_t ohD = take((3 * sizeof(GemmArgs) + sizeof(double) - 1) / sizeof(double) + 2);
     double *base = nullptr;
     if (cudaMalloc(&base, off * sizeof(double)) != cudaSuccess) return SGP_ENOMEM;
     cudaMemset(base, 0, off * sizeof(double));
@@ -1719,6 +1745,7 @@ static int lg_alloc(const ModelDev &M, LgPtrs &L, void **owner) {
     L.bjPart = base + obP;
     L.bjCnt = reinterpret_cast<int *>(base + obC);
     L.bjDesc = reinterpret_cast<GemmArgs *>(base + ((obD + 1) & ~size_t(1)));  // 16-byte aligned
+    L.hdesc = reinterpret_cast<GemmArgs *>(base + ((ohD + 1) & ~size_t(1)));
     {
         L.bj_hs = nullptr;
         for (cudaEvent_t &e : L.bj_ev) e = nullptr;

@@ -205,7 +205,12 @@ _DEVICE_CACHE_MAX = 8
 
 
 def _fingerprint(model, data):
+    import os
+
     h = hashlib.sha1()
+    # the test-only SGP_FORCE_LARGE hook routes a model through the large-d path; a device
+    # model that served one routing is not reused for the other
+    h.update(os.environ.get("SGP_FORCE_LARGE", "").encode())
     for a in (data.x, data.y):
         a = np.ascontiguousarray(np.asarray(a, dtype=float))
         h.update(str(a.shape).encode())
