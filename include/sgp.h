@@ -136,7 +136,11 @@ typedef struct sgp_chain_config {
     int warm_order;     /* SGP_ORDER_* of warm decompositions (dynamic_eigendecompose) */
     int cold_order;     /* SGP_ORDER_* of cold decompositions (static_eigendecompose); the
                            fused small-d kernel always uses the reference order */
+    int path;           /* SGP_PATH_AUTO: one CTA per chain for d <= 256, the large path above;
+                           SGP_PATH_LATENCY: every chain on the whole GPU (large path) */
 } sgp_chain_config;
+#define SGP_PATH_AUTO 0
+#define SGP_PATH_LATENCY 1
 
 /* Per-move records (ChainRecord, sampler.py:86-99), arrays of moves*Z
  * (index move*Z + z); d_rec_q is moves*Z*d or NULL. */

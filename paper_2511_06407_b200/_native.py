@@ -36,6 +36,7 @@ TRANSFORM_IDENTITY = 1
 
 METRIC_CODES = {"softabs-dynamic": 0, "softabs-static": 1, "euclidean": 2}
 ORDER_CODES = {"cyclic": 0, "parallel": 1, "refine": 2}
+PATH_CODES = {"auto": 0, "latency": 1}
 
 EVAL_POTENTIAL = 1
 EVAL_GRADIENT = 2
@@ -88,7 +89,7 @@ class ChainConfigC(ctypes.Structure):
     _fields_ = [("epsilon", ctypes.c_double), ("leapfrogs", ctypes.c_int), ("kappa", ctypes.c_double),
                 ("zeta", ctypes.c_double), ("fp_max_iters", ctypes.c_int), ("fp_tol", ctypes.c_double),
                 ("gs_interval", ctypes.c_int), ("sweep_cap", ctypes.c_int), ("metric", ctypes.c_int),
-                ("warm_order", ctypes.c_int), ("cold_order", ctypes.c_int)]
+                ("warm_order", ctypes.c_int), ("cold_order", ctypes.c_int), ("path", ctypes.c_int)]
 
 
 class GridSpecC(ctypes.Structure):

@@ -738,7 +738,7 @@ extern "C" int sgp_leapfrog(const sgp_model *m, const sgp_chain_config *cfg, con
                             sgp_leapfrog_diag *diag, void *stream) {
     if (!m || !cfg || !st || !d_p || st->n_chains < 1) return SGP_EINVAL;
     if (cfg->fp_max_iters < 1 || cfg->fp_max_iters > 32) return SGP_EINVAL;
-    if (lg_is_large(m->dev)) {
+    if (lg_is_large(m->dev) || lg_route_latency(m->dev, *cfg)) {
         const LgPtrs *L = large_ws(m);
         if (!L) return SGP_ENOMEM;
         return lg_leapfrog_api(*L, cfg, st, d_p, diag, S(stream));
@@ -778,7 +778,7 @@ __global__ void __launch_bounds__(SGP_MAX_NT) k_chain_init(ModelDev M, SmemPlan 
 extern "C" int sgp_chain_init(const sgp_model *m, const sgp_chain_config *cfg, const sgp_chain_state *st,
                               void *stream) {
     if (!m || !cfg || !st || st->n_chains < 1) return SGP_EINVAL;
-    if (lg_is_large(m->dev)) {
+    if (lg_is_large(m->dev) || lg_route_latency(m->dev, *cfg)) {
         const LgPtrs *L = large_ws(m);
         if (!L) return SGP_ENOMEM;
         return lg_chain_init(*L, cfg, st, S(stream));
@@ -899,7 +899,7 @@ extern "C" int sgp_run_moves(const sgp_model *m, const sgp_chain_config *cfg, co
         !rec->wall_ms)
         return SGP_EINVAL;
     if (moves == 0) return SGP_OK;
-    if (lg_is_large(m->dev)) {
+    if (lg_is_large(m->dev) || lg_route_latency(m->dev, *cfg)) {
         const LgPtrs *LW = large_ws(m);
         if (!LW) return SGP_ENOMEM;
         return lg_run_moves(*LW, cfg, st, moves, move_offset, d_z, d_logu, rec, S(stream));

@@ -1682,6 +1682,18 @@ static int lg_leapfrog(LgCtx &c, int &f, int *fp_p, int *fp_q, double *sweep_sum
 
 // d > 256 (or very wide designs) take the GEMM path; SGP_FORCE_LARGE=1 routes
 // any model through it (used by the parity tests on the golden chains).
+// Latency path (ChainConfig.path = "latency", SGP_PATH_LATENCY): each chain's leapfrog runs on
+// the whole GPU through the large path (DMMA GEMMs, the grid-wide reference-order Jacobi or the
+// refinement) instead of one CTA per chain; chains of the batch run one after the other.
+// Measured single-chain ms per leapfrog (tools/latency_single_chain.py, profiles/r2_latency.md),
+// one CTA vs latency path: d = 83 cyclic 16.2 / 14.9, parallel 15.1 / 4.6; d = 163 cyclic
+// 78 / 24, parallel 75 / 4.3; at d = 34 one CTA is faster (2.7 ms).  Opt-in, because the two
+// paths agree with the reference to 1e-9 but not bit for bit with each other, and the default
+// keeps a chain's bits independent of the batch it runs in.
+static bool lg_route_latency(const ModelDev &M, const sgp_chain_config &cfg) {
+    return cfg.path == SGP_PATH_LATENCY && M.mp.lik != SGP_LIK_QUADRATIC;
+}
+
 static bool lg_is_large(const ModelDev &M) {
     if (M.mp.lik == SGP_LIK_QUADRATIC) return false;
     const char *f = getenv("SGP_FORCE_LARGE");

@@ -79,10 +79,13 @@ def test_cold_eigh_bit_exact(model_case):
     np.testing.assert_array_equal(psi, psi_o)
 
 
-def test_short_chain_matches_oracle(model_case):
+@pytest.mark.parametrize("path", ["auto", "latency"])
+def test_short_chain_matches_oracle(model_case, path):
+    """One CTA per chain (auto) and the whole-GPU latency path both reproduce the reference
+    algorithm's chain (reference pivot order)."""
     name, model, data, target = model_case
     eps = 0.002
-    cfg = S.ChainConfig(epsilon=eps, leapfrogs=4, moves=5, burnin=0, seed=11, record_q=True)
+    cfg = S.ChainConfig(epsilon=eps, leapfrogs=4, moves=5, burnin=0, seed=11, record_q=True, path=path)
     try:
         ref = oracle.run_chain(oracle.OTarget(model, data),
                                oracle.OConfig(epsilon=eps, leapfrogs=4, moves=5, burnin=0, seed=11,
