@@ -235,6 +235,19 @@ int sgp_run_moves(const sgp_model *model, const sgp_chain_config *cfg,
                   const double *d_z, const double *d_logu, sgp_move_records *rec,
                   void *stream);
 
+/* The thermodynamic-integration ladder walk of every chain in ONE launch (replaces
+ * evidence.py:142-163 _ladder_walk): for rung s = 0..n_rungs-1 each chain's
+ * target moves to d_taus[s], its frame is rebuilt cold at its current position (a rung is a new
+ * run_chain, sampler.py:322-328), moves_per_rung moves run with the rung's draws, and
+ * d_values[z * n_rungs + s] = log_likelihood at the rung's end (posterior.py:277-279), or the
+ * average over the rung's moves when rung_average.  d_z: n_rungs*moves*Z*d normals,
+ * d_logu: n_rungs*moves*Z log-uniforms, in the reference's per-rung RNG order.  A chain that
+ * fails (status != 0) stops; its remaining values are untouched.  One CTA per chain: models on
+ * the large path (d > 256 or path = latency) return SGP_EINVAL and are walked rung by rung. */
+int sgp_ladder_walk(const sgp_model *model, const sgp_chain_config *cfg, const sgp_chain_state *st,
+                    int n_rungs, const double *d_taus, int moves_per_rung, int rung_average,
+                    const double *d_z, const double *d_logu, double *d_values, void *stream);
+
 /* Laplace-grid evidence oracle (replaces evidence.py:330-426
  * laplace_grid_oracle's node loop).  The grid of
  * (c_g, sigma_g) midpoints is round(c_max/c_mesh) x round(sigma_max/sigma_mesh)

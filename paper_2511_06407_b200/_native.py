@@ -17,6 +17,7 @@ LIB_PATH = os.path.join(HERE, "libsgp.so")
 
 # return / status codes (include/sgp.h)
 SGP_OK = 0
+SGP_EINVAL = -1
 STATUS_OK = 0
 STATUS_DIVERGENCE = 1
 STATUS_DOMAIN = 2
@@ -155,6 +156,8 @@ def lib():
         "sgp_chain_init": (i, [vp, ctypes.POINTER(ChainConfigC), ctypes.POINTER(ChainState), vp]),
         "sgp_run_moves": (i, [vp, ctypes.POINTER(ChainConfigC), ctypes.POINTER(ChainState), i, i, vp,
                               vp, ctypes.POINTER(MoveRecords), vp]),
+        "sgp_ladder_walk": (i, [vp, ctypes.POINTER(ChainConfigC), ctypes.POINTER(ChainState), i, vp, i, i, vp,
+                                vp, vp, vp]),
         "sgp_device_info": (i, [c_ip, c_ip, c_ip]),
         "sgp_version": (ctypes.c_char_p, []),
         "sgp_debug_phase_cycles": (i, [vp, i]),

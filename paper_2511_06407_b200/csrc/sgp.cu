@@ -792,11 +792,18 @@ extern "C" int sgp_chain_init(const sgp_model *m, const sgp_chain_config *cfg, c
 }
 
 // The MH move loop (sampler.py:355-411), C leapfrogs per move, all on device.
+// n_rungs > 0: the whole thermodynamic-integration ladder walk of a chain in the same launch
+// (evidence.py:142-163): for every rung s the chain's target moves to taus[s], the frame is
+// rebuilt cold at the current position (each rung is a new run_chain: _initial_frame,
+// sampler.py:322-328), `moves` moves run with the rung's draws (dz/dlogu indexed by rung), and
+// values[z * n_rungs + s] = log_likelihood at the rung's end (posterior.py:277-279), or its
+// average over the rung's moves when rung_average.  Per-move records are optional then.
 template <int NT, int MINB>
 __global__ void __launch_bounds__(NT, MINB) k_run_moves(ModelDev M, SmemPlan pl, sgp_chain_config cfg,
                                                       sgp_chain_state st, int moves, int move_offset,
                                                       const double *dz, const double *dlogu, sgp_move_records rec,
-                                                      size_t spc) {
+                                                      size_t spc, int n_rungs, const double *taus,
+                                                      int rung_average, double *values) {
     const int z = blockIdx.x;
     const int Z = st.n_chains;
     const int d = M.mp.d;
@@ -805,78 +812,114 @@ __global__ void __launch_bounds__(NT, MINB) k_run_moves(ModelDev M, SmemPlan pl,
     EvalCtx E;
     setup_ws(w, E, sgp_smem, pl, M, st.scratch + (size_t)z * spc);
     if (st.status[z] != 0) return;
-    const double tau = st.tau[z];
     const bool euclid = cfg.metric == SGP_METRIC_EUCLIDEAN;
     for (int j = threadIdx.x; j < d; j += SGP_NT) w.q0[j] = st.q[(size_t)z * d + j];
     __syncthreads();
     int f = 0;
-    int s = frame_resume(w, E, cfg, tau, st.psi + z * dd, st.lam + (size_t)z * d, st.since[z], f);
-    if (s) {
-        if (threadIdx.x == 0) st.status[z] = SGP_STATUS_CHAIN_START;
-        return;
+    if (n_rungs == 0) {
+        int s = frame_resume(w, E, cfg, st.tau[z], st.psi + z * dd, st.lam + (size_t)z * d, st.since[z], f);
+        if (s) {
+            if (threadIdx.x == 0) st.status[z] = SGP_STATUS_CHAIN_START;
+            return;
+        }
     }
     int final_status = 0;
-    for (int mv = 0; mv < moves; ++mv) {
-        const unsigned long long t0 = globaltimer_ns();
-        const double *zz = dz + ((size_t)mv * Z + z) * d;
-        if (euclid) {
-            for (int j = threadIdx.x; j < d; j += SGP_NT) w.p[j] = zz[j];
-            __syncthreads();
-        } else {
-            for (int j = threadIdx.x; j < d; j += SGP_NT) w.pn[j] = zz[j];
-            __syncthreads();
-            metric_apply(w.p, w.tmp, w.P[f], w.g[f], w.pn, d, 2);
-        }
-        const double pot_before = w.sc[2];
-        const double h_before = pot_before + frame_kinetic(w, E, cfg, f);
-        for (int j = threadIdx.x; j < d; j += SGP_NT) w.qs[j] = w.q0[j];
-        __syncthreads();
-        LFDiag dg;
-        dg.fp_p = dg.fp_q = dg.nsweep = dg.sweep_cnt = 0;
-        dg.sweep_sum = 0.0;
-        dg.sweeps = nullptr;
-        int fr = f;
-        int ls = 0;
-        for (int l = 0; l < cfg.leapfrogs; ++l) {
-            ls = euclid ? leapfrog_euclid(w, E, cfg, tau) : leapfrog_riemann(w, E, cfg, tau, fr, dg);
-            if (ls) break;
-        }
-        bool div = ls != 0;
-        double h_after = NAN;
-        if (!div) {
-            h_after = w.sc[2] + frame_kinetic(w, E, cfg, fr);
-            if (!isfinite(h_after)) div = true;
-        }
-        if (div) h_after = NAN;
-        const bool accept = !div && (h_before - h_after) > dlogu[(size_t)mv * Z + z];
-        __syncthreads();
-        if (threadIdx.x == 0) *E.status = 0;
-        __syncthreads();
-        if (accept) {
-            f = fr;
-        } else {
-            if (div && mv + move_offset == 0) {
-                final_status = SGP_STATUS_FIRST_MOVE;
-            } else {
-                for (int j = threadIdx.x; j < d; j += SGP_NT) w.q0[j] = w.qs[j];
-                __syncthreads();
-                int rs = frame_build(w, E, cfg, tau, f);  // cold resync (sampler.py:392-397)
-                if (rs) final_status = rs;
+    const int rungs = n_rungs > 0 ? n_rungs : 1;
+    for (int rg = 0; rg < rungs && !final_status; ++rg) {
+        const double tau = n_rungs > 0 ? taus[rg] : st.tau[z];
+        if (n_rungs > 0) {
+            if (frame_build(w, E, cfg, tau, f)) {  // rung start: a cold frame (sampler.py:322-328)
+                final_status = SGP_STATUS_CHAIN_START;
+                break;
             }
         }
-        const size_t ri = (size_t)mv * Z + z;
-        if (threadIdx.x == 0) {
-            rec.logpost[ri] = -w.sc[2];
-            rec.h_before[ri] = h_before;
-            rec.h_after[ri] = h_after;
-            rec.accept[ri] = accept;
-            rec.divergent[ri] = div;
-            rec.sweeps_mean[ri] = dg.sweep_cnt ? dg.sweep_sum / dg.sweep_cnt : 0.0;
-            rec.wall_ms[ri] = (double)(globaltimer_ns() - t0) * 1e-6;
+        double ll_sum = 0.0;
+        const size_t moff = (size_t)rg * moves;
+        // log_likelihood(q) = -sum_i U_i (posterior.py:277-279); the frame carries it except at
+        // tau = 0, where the tempered state skips the likelihood: evaluate it separately then
+        // (sum only; the trace ignores the per-sample fields at tau = 0) and keep the frame's U
+        auto loglik = [&]() -> double {
+            if (tau != 0.0) return -w.sc[3];
+            const double pot = w.sc[2];
+            eval_at(w, E, w.q0, tau, SGP_EVAL_SUMPOT);
+            const double ll = -w.sc[3];
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                w.sc[2] = pot;
+                *E.status = 0;
+            }
+            __syncthreads();
+            return ll;
+        };
+        for (int mv = 0; mv < moves; ++mv) {
+            const unsigned long long t0 = globaltimer_ns();
+            const double *zz = dz + ((moff + mv) * Z + z) * d;
+            if (euclid) {
+                for (int j = threadIdx.x; j < d; j += SGP_NT) w.p[j] = zz[j];
+                __syncthreads();
+            } else {
+                for (int j = threadIdx.x; j < d; j += SGP_NT) w.pn[j] = zz[j];
+                __syncthreads();
+                metric_apply(w.p, w.tmp, w.P[f], w.g[f], w.pn, d, 2);
+            }
+            const double pot_before = w.sc[2];
+            const double h_before = pot_before + frame_kinetic(w, E, cfg, f);
+            for (int j = threadIdx.x; j < d; j += SGP_NT) w.qs[j] = w.q0[j];
+            __syncthreads();
+            LFDiag dg;
+            dg.fp_p = dg.fp_q = dg.nsweep = dg.sweep_cnt = 0;
+            dg.sweep_sum = 0.0;
+            dg.sweeps = nullptr;
+            int fr = f;
+            int ls = 0;
+            for (int l = 0; l < cfg.leapfrogs; ++l) {
+                ls = euclid ? leapfrog_euclid(w, E, cfg, tau) : leapfrog_riemann(w, E, cfg, tau, fr, dg);
+                if (ls) break;
+            }
+            bool div = ls != 0;
+            double h_after = NAN;
+            if (!div) {
+                h_after = w.sc[2] + frame_kinetic(w, E, cfg, fr);
+                if (!isfinite(h_after)) div = true;
+            }
+            if (div) h_after = NAN;
+            const bool accept = !div && (h_before - h_after) > dlogu[(moff + mv) * Z + z];
+            __syncthreads();
+            if (threadIdx.x == 0) *E.status = 0;
+            __syncthreads();
+            if (accept) {
+                f = fr;
+            } else {
+                // a divergence on a run_chain's first move raises ChainError (sampler.py:388-391);
+                // every rung of a ladder walk is its own run_chain
+                if (div && (n_rungs > 0 ? mv : mv + move_offset) == 0) {
+                    final_status = SGP_STATUS_FIRST_MOVE;
+                } else {
+                    for (int j = threadIdx.x; j < d; j += SGP_NT) w.q0[j] = w.qs[j];
+                    __syncthreads();
+                    int rs = frame_build(w, E, cfg, tau, f);  // cold resync (sampler.py:392-397)
+                    if (rs) final_status = rs;
+                }
+            }
+            if (n_rungs > 0 && rung_average && !final_status) ll_sum += loglik();  // at the recorded q
+            const size_t ri = (moff + mv) * Z + z;
+            if (threadIdx.x == 0 && rec.logpost) {
+                rec.logpost[ri] = -w.sc[2];
+                rec.h_before[ri] = h_before;
+                rec.h_after[ri] = h_after;
+                rec.accept[ri] = accept;
+                rec.divergent[ri] = div;
+                rec.sweeps_mean[ri] = dg.sweep_cnt ? dg.sweep_sum / dg.sweep_cnt : 0.0;
+                rec.wall_ms[ri] = (double)(globaltimer_ns() - t0) * 1e-6;
+            }
+            if (rec.q)
+                for (int j = threadIdx.x; j < d; j += SGP_NT) rec.q[ri * d + j] = (final_status ? w.qs[j] : w.q0[j]);
+            if (final_status) break;
         }
-        if (rec.q)
-            for (int j = threadIdx.x; j < d; j += SGP_NT) rec.q[ri * d + j] = (final_status ? w.qs[j] : w.q0[j]);
-        if (final_status) break;
+        if (n_rungs > 0 && !final_status) {
+            const double v = rung_average ? ll_sum / moves : loglik();
+            if (threadIdx.x == 0) values[(size_t)z * n_rungs + rg] = v;
+        }
     }
     __syncthreads();
     for (int j = threadIdx.x; j < d; j += SGP_NT) st.q[(size_t)z * d + j] = w.q0[j];
@@ -890,19 +933,42 @@ __global__ void __launch_bounds__(NT, MINB) k_run_moves(ModelDev M, SmemPlan pl,
     }
 }
 
+static int launch_moves(const sgp_model *m, const sgp_chain_config *cfg, const sgp_chain_state *st, int moves,
+                        int move_offset, const double *d_z, const double *d_logu, const sgp_move_records *rec,
+                        int n_rungs, const double *d_taus, int rung_average, double *d_values, void *stream);
+
 extern "C" int sgp_run_moves(const sgp_model *m, const sgp_chain_config *cfg, const sgp_chain_state *st, int moves,
                              int move_offset, const double *d_z, const double *d_logu, sgp_move_records *rec,
                              void *stream) {
     if (!m || !cfg || !st || !rec || st->n_chains < 1 || moves < 0 || !d_z || !d_logu) return SGP_EINVAL;
-    if (cfg->fp_max_iters < 1 || cfg->leapfrogs < 1) return SGP_EINVAL;
     if (!rec->logpost || !rec->h_before || !rec->h_after || !rec->accept || !rec->divergent || !rec->sweeps_mean ||
         !rec->wall_ms)
         return SGP_EINVAL;
+    return launch_moves(m, cfg, st, moves, move_offset, d_z, d_logu, rec, 0, nullptr, 0, nullptr, stream);
+}
+
+extern "C" int sgp_ladder_walk(const sgp_model *m, const sgp_chain_config *cfg, const sgp_chain_state *st,
+                               int n_rungs, const double *d_taus, int moves_per_rung, int rung_average,
+                               const double *d_z, const double *d_logu, double *d_values, void *stream) {
+    if (!m || !cfg || !st || st->n_chains < 1 || n_rungs < 1 || moves_per_rung < 1 || !d_taus || !d_z || !d_logu ||
+        !d_values)
+        return SGP_EINVAL;
+    if (lg_is_large(m->dev) || lg_route_latency(m->dev, *cfg)) return SGP_EINVAL;  // the caller walks rung by rung
+    sgp_move_records none{};
+    return launch_moves(m, cfg, st, moves_per_rung, 0, d_z, d_logu, &none, n_rungs, d_taus, rung_average, d_values,
+                        stream);
+}
+
+static int launch_moves(const sgp_model *m, const sgp_chain_config *cfg, const sgp_chain_state *st, int moves,
+                        int move_offset, const double *d_z, const double *d_logu, const sgp_move_records *rec,
+                        int n_rungs, const double *d_taus, int rung_average, double *d_values, void *stream) {
+    if (cfg->fp_max_iters < 1 || cfg->leapfrogs < 1) return SGP_EINVAL;
     if (moves == 0) return SGP_OK;
     if (lg_is_large(m->dev) || lg_route_latency(m->dev, *cfg)) {
         const LgPtrs *LW = large_ws(m);
         if (!LW) return SGP_ENOMEM;
-        return lg_run_moves(*LW, cfg, st, moves, move_offset, d_z, d_logu, rec, S(stream));
+        return lg_run_moves(*LW, cfg, st, moves, move_offset, d_z, d_logu, const_cast<sgp_move_records *>(rec),
+                            S(stream));
     }
     const ChainLaunch L = chain_launch(m);
     const size_t spc = sgp_scratch_doubles(m);
@@ -910,8 +976,8 @@ extern "C" int sgp_run_moves(const sgp_model *m, const sgp_chain_config *cfg, co
 #define SGP_LAUNCH_MOVES(NT_, MB_)                                                                        \
     rc = launch_prep(k_run_moves<NT_, MB_>, L.pl.bytes);                                                 \
     if (rc) return rc;                                                                                    \
-    k_run_moves<NT_, MB_><<<st->n_chains, NT_, L.pl.bytes, S(stream)>>>(m->dev, L.pl, *cfg, *st, moves,    \
-                                                                        move_offset, d_z, d_logu, *rec, spc)
+    k_run_moves<NT_, MB_><<<st->n_chains, NT_, L.pl.bytes, S(stream)>>>(                                   \
+        m->dev, L.pl, *cfg, *st, moves, move_offset, d_z, d_logu, *rec, spc, n_rungs, d_taus, rung_average, d_values)
     if (L.nt == 32) {
         SGP_LAUNCH_MOVES(32, 12);
     } else if (L.nt == 64) {

@@ -155,6 +155,9 @@ def device_ladder_runner(target, chain_seqs, q_warm, ladder, config, rung_averag
     if spread_moves > 0 and alive:
         step(target, dataclasses.replace(config, moves=spread_moves, burnin=0, record_q=False),
              lambda k: subs[k][0])
+    if alive and _resident_walk(target, ladder, config, rung_average, subs, q, alive, values, errors):
+        return values, errors
+    # the large path: rung by rung (one cold start + one move loop per rung for all chains)
     for s, tau in enumerate(ladder.taus):
         if not alive:
             break
@@ -173,6 +176,61 @@ def device_ladder_runner(target, chain_seqs, q_warm, ladder, config, rung_averag
         if errors[k] is not None:
             values[k] = np.nan
     return values, errors
+
+
+def _resident_walk(target, ladder, config, rung_average, subs, q, alive, values, errors):
+    """The whole ladder walk of the alive chains in one device launch (sgp_ladder_walk: per rung
+    a cold start at the rung's temperature and the rung's moves, evidence.py:142-163).  The
+    draws are the reference's: chain k, rung s from default_rng(subs[k][s + 1]), d normals then
+    one uniform per move.  Returns False when the model runs on the large path."""
+    import torch
+
+    from . import _native as nat
+    from .sampler import DeviceChains, draw_move_randoms
+
+    if getattr(target.device, "is_quadratic", False):
+        return False
+    S, A, d = ladder.size, ladder.moves_per_rung, target.dim
+    cfg = dataclasses.replace(config, moves=A, leapfrogs=ladder.leapfrogs, burnin=0, record_q=False)
+    Z = len(alive)
+    zs = np.empty((S, A, Z, d))
+    us = np.empty((S, A, Z))
+    for j, k in enumerate(alive):
+        for s in range(S):
+            zk, uk = draw_move_randoms(np.random.default_rng(subs[k][s + 1]), A, d)
+            zs[s, :, j] = zk
+            us[s, :, j] = uk
+    chains = DeviceChains(target.device, np.full(Z, float(ladder.taus[0])), cfg)
+    chains.set_q(q[alive])
+    taus = nat.dev_f64(np.asarray(ladder.taus, dtype=float))
+    out = torch.full((Z, S), float("nan"), dtype=torch.float64, device="cuda")
+    with np.errstate(divide="ignore"):
+        lu = np.log(us)
+    tz, tl = nat.dev_f64(zs), nat.dev_f64(lu)
+    rc = chains.L.sgp_ladder_walk(target.device.handle, chains.ccfg, chains.cstate, int(S), nat.ptr(taus), int(A),
+                                  int(bool(rung_average)), nat.ptr(tz), nat.ptr(tl), nat.ptr(out), nat.stream())
+    if rc == nat.SGP_EINVAL:
+        return False
+    nat.check(rc, "sgp_ladder_walk")
+    status = chains.status_host()
+    vals = out.cpu().numpy()
+    qf = chains.q.cpu().numpy()
+    for j, k in enumerate(alive):
+        if status[j] == nat.STATUS_FIRST_MOVE:
+            errors[k] = "divergence on the first move; initial point or epsilon unusable"
+        elif status[j] == nat.STATUS_CHAIN_START:
+            errors[k] = "chain start failed: non-finite or invalid initial state"
+        elif status[j] == nat.STATUS_JACOBI:
+            raise JacobiError("cold resync failed to converge")
+        elif status[j] != 0:
+            raise ChainError(f"chain failed with status {status[j]}")
+        else:
+            values[k] = vals[j]
+            q[k] = qf[j]
+    for k in range(len(errors)):
+        if errors[k] is not None:
+            values[k] = np.nan
+    return True
 
 
 def _dist_info():

@@ -224,3 +224,20 @@ def test_unit_sharding_is_bitwise_identical(world):
                 np.testing.assert_array_equal(rvs[k], ref[k].rung_values)
                 assert bmes[k] == ref[k].bme_mean
             np.testing.assert_array_equal(rh, ref_rh)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("rung_average", [False, True])
+def test_resident_ladder_walk_equals_rung_by_rung(rung_average, monkeypatch):
+    """sgp_ladder_walk (the whole walk in one launch) == one launch per rung (the large-path
+    fallback of device_ladder_runner), with and without rung averaging."""
+    from paper_2511_06407_b200.posterior import PosteriorTarget
+    g, model, data = case("ti_small")
+    ladder = E.TemperLadder(taus=g["taus"], moves_per_rung=3, leapfrogs=5, chains=3)
+    cfg = ChainConfig(epsilon=0.02, leapfrogs=5, moves=10, burnin=0, seed=123)
+    kw = dict(warmup_segment_moves=10, warmup_max_segments=2, spread_moves=2, rung_average=rung_average,
+              target=PosteriorTarget(model, data))
+    resident = E.thermo_integrate(model, data, ladder, cfg, **kw)
+    monkeypatch.setattr(E, "_resident_walk", lambda *a, **k: False)
+    per_rung = E.thermo_integrate(model, data, ladder, cfg, **kw)
+    assert rel_err(resident.rung_values, per_rung.rung_values) < 1e-12
