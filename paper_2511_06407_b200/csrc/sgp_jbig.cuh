@@ -59,6 +59,18 @@ struct JbArgs {
     double skip;
 };
 
+#ifdef SGP_JBIG_PROF
+// phase cycles of the chain CTA (summed over windows): 0 chain warp in its window, 1 chain warp
+// at the start barrier, 2 lookahead total, 3 lookahead owner wait, 4 io publish, 5 io deferred
+// load, 6 io prefetch, 7 end barrier wait (warp 0), 8 windows
+__device__ unsigned long long jb_prof[16];
+#define JB_T0(v) const long long v = clock64()
+#define JB_ACC(i, v) atomicAdd(&jb_prof[i], (unsigned long long)(clock64() - (v)))
+#else
+#define JB_T0(v)
+#define JB_ACC(i, v)
+#endif
+
 __device__ __forceinline__ unsigned jb_ld_acquire(const unsigned *p) {
     unsigned v;
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -81,13 +93,21 @@ __device__ __forceinline__ unsigned jb_need_diag(int m, unsigned prev_start, int
     return prev_start + (unsigned)min(m + 2, prev_nw - 1);
 }
 
-// wait until every owner has completed window `need` (io or lookahead warp, warp-uniform)
-__device__ __forceinline__ void jb_wait_owners(const JbArgs &a, unsigned need) {
-    if (need == 0u) return;
+// wait until every owner has completed window `need` (one warp, warp-uniform).  *cache holds
+// the smallest owner progress this warp last observed with an acquire load; while it covers
+// `need` nothing is polled (the earlier acquire already ordered the data behind it).
+__device__ __forceinline__ void jb_wait_owners(const JbArgs &a, unsigned need, volatile unsigned *cache) {
+    if (need == 0u || *cache >= need) return;
     const int lane = threadIdx.x & 31;
     for (;;) {
         const unsigned v = lane < a.nown ? jb_ld_acquire(a.prog + lane) : 0xffffffffu;
-        if (__all_sync(0xffffffffu, v >= need)) break;
+        unsigned mn = v;
+        for (int o = 16; o; o >>= 1) mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+        if (mn >= need) {
+            if (lane == 0) *cache = mn;
+            __syncwarp();
+            break;
+        }
         __nanosleep(64);
     }
 }
@@ -102,6 +122,7 @@ struct JbShared {
     int *rf[2];                    // [32]
     double *rnext, *rfin;          // [32] lookahead -> chain, chain -> io
     volatile int *cnt;             // rotations of the current window published by the chain
+    volatile unsigned *own_la, *own_io;  // owner-progress caches of the lookahead and io warps
 };
 
 __device__ __forceinline__ void jb_chain_window(const JbArgs &a, const JbShared &sh, int p, int m, unsigned seq,
@@ -122,6 +143,8 @@ __device__ __forceinline__ void jb_chain_window(const JbArgs &a, const JbShared 
     double piv = __shfl_sync(0xffffffffu, r, 0);
     double aqq = __shfl_sync(0xffffffffu, dq, 0);
     const double skip = a.skip;
+    double my_c = 1.0, my_s = 0.0;
+    int my_f = 0;
     // pending rotation j-1, applied to the lanes while rotation j's parameters are computed
     bool has = false;
     double pc = 1.0, ps = 0.0, pdq = 0.0;
@@ -163,12 +186,10 @@ __device__ __forceinline__ void jb_chain_window(const JbArgs &a, const JbShared 
         } else {
             piv = X;
         }
-        if (lane == 0) {
-            rc[j] = c;
-            rs[j] = s;
-            rf[j] = rot ? 1 : 0;
-            __threadfence_block();
-            *sh.cnt = (int)(seq * 64u) + j + 1;
+        if (lane == j) {  // rotation j's parameters stay with lane j until the window ends
+            my_c = c;
+            my_s = s;
+            my_f = rot ? 1 : 0;
         }
         has = rot;
         pc = c;
@@ -183,6 +204,10 @@ __device__ __forceinline__ void jb_chain_window(const JbArgs &a, const JbShared 
         sh.rfin[(seq & 1) * JB_W + lane] = r;
         sh.dg[k] = dq;
     }
+    // the window's rotation ring, written once (the lookahead folds it after the window)
+    rc[lane] = my_c;
+    rs[lane] = my_s;
+    rf[lane] = lane < n ? my_f : 0;
 }
 
 // Lookahead warp at window (p, m): rows W_{m+1}.  Their running a_kp must enter the chain's
@@ -193,12 +218,17 @@ __device__ __forceinline__ void jb_lookahead(const JbArgs &a, const JbShared &sh
                                              unsigned start, unsigned prev_start, int prev_nw) {
     const int d = a.d, lane = threadIdx.x & 31;
     const int q0 = p + 1 + JB_W * m, n = min(JB_W, d - q0);
-    if (q0 + JB_W >= d) return;  // no next window in this pass
+    if (q0 + JB_W >= d) {  // no next window in this pass
+        asm volatile("bar.sync 4, 64;" ::: "memory");
+        return;
+    }
     const int k = q0 + JB_W + lane;
     const bool valid = k < d;
     unsigned need = jb_need_diag(m, prev_start, prev_nw);
     if (m >= 2) need = max(need, start + (unsigned)(m - 2));
-    jb_wait_owners(a, need);
+    JB_T0(tw);
+    jb_wait_owners(a, need, sh.own_la);
+    if (lane == 0) JB_ACC(3, tw);
     double *rowk = a.L + (size_t)(valid ? k : d - 1) * d;
     double r = 0.0;
     if (valid) r = (m <= 1) ? __ldcg(rowk + p) : __ldcg(a.R + k);
@@ -223,36 +253,32 @@ __device__ __forceinline__ void jb_lookahead(const JbArgs &a, const JbShared &sh
             for (int j = 0; j < JB_W; ++j) __stcg(seg + j, e[j]);
         }
     }
-    {  // follow window m
-        const volatile double *rc = sh.rc[seq & 1], *rs = sh.rs[seq & 1];
-        const volatile int *rf = sh.rf[seq & 1];
+    {  // window m: its tile is loaded while the chain runs, folded once the chain is done
         double *seg = rowk + q0;
         double e[JB_W];
 #pragma unroll
         for (int j = 0; j < JB_W; ++j) e[j] = (valid && j < n) ? __ldcg(seg + j) : 0.0;
-        const int base = (int)(seq * 64u);
+        asm volatile("bar.sync 4, 64;" ::: "memory");  // the chain wrote the window's ring
+        const double *rc = sh.rc[seq & 1], *rs = sh.rs[seq & 1];
+        const int *rf = sh.rf[seq & 1];
 #pragma unroll
         for (int j = 0; j < JB_W; ++j) {
-            if (j < n) {
-                while (*sh.cnt < base + j + 1) {
-                }
-                __threadfence_block();
-                if (rf[j]) {
-                    const double c = rc[j], s = rs[j];
-                    const double akp = r, akq = e[j];
-                    r = __dsub_rn(__dmul_rn(c, akp), __dmul_rn(s, akq));
-                    e[j] = __dadd_rn(__dmul_rn(s, akp), __dmul_rn(c, akq));
-                }
+            if (j < n && rf[j]) {
+                const double c = rc[j], s = rs[j];
+                const double akp = r, akq = e[j];
+                r = __dsub_rn(__dmul_rn(c, akp), __dmul_rn(s, akq));
+                e[j] = __dadd_rn(__dmul_rn(s, akp), __dmul_rn(c, akq));
             }
         }
         if (valid) {
+            sh.rnext[lane] = r;
 #pragma unroll
             for (int j = 0; j < JB_W; ++j)
                 if (j < n) __stcg(seg + j, e[j]);
-            sh.rnext[lane] = r;
         }
     }
-    __threadfence();
+    // no fence here: these stores are ordered before the io warps' fence and release of this
+    // window by the CTA barrier that ends it (happens-before is transitive across the scopes)
 }
 
 // io warps (64 threads): write window (p, m) of the chain back and publish it as `seq`
@@ -285,9 +311,17 @@ __device__ __forceinline__ void jb_publish(const JbArgs &a, const JbShared &sh, 
 __device__ __forceinline__ void jb_load_diag(const JbArgs &a, double *B, int p, int m, int io_t) {
     const int d = a.d;
     const int q0 = p + 1 + JB_W * m, n = min(JB_W, d - q0);
-    for (int idx = io_t; idx < JB_W * JB_W; idx += 64) {
-        const int l = idx >> 5, j = idx & 31;
-        if (j < l && l < n) B[l * JB_LDB + j] = __ldcg(a.L + (size_t)(q0 + l) * d + q0 + j);
+    // all 16 loads of a thread in flight before the stores (one L2 round trip, not 16)
+    double v[JB_W * JB_W / 64];
+#pragma unroll
+    for (int t = 0; t < JB_W * JB_W / 64; ++t) {
+        const int idx = io_t + 64 * t, l = idx >> 5, j = idx & 31;
+        v[t] = (j < l && l < n) ? __ldcg(a.L + (size_t)(q0 + l) * d + q0 + j) : 0.0;
+    }
+#pragma unroll
+    for (int t = 0; t < JB_W * JB_W / 64; ++t) {
+        const int idx = io_t + 64 * t, l = idx >> 5, j = idx & 31;
+        if (j < l && l < n) B[l * JB_LDB + j] = v[t];
     }
 }
 
@@ -314,8 +348,14 @@ __device__ void jb_chain_cta(const JbArgs &a, double *smem) {
     sh.rf[0] = reinterpret_cast<int *>(q);
     sh.rf[1] = sh.rf[0] + JB_W;
     sh.cnt = reinterpret_cast<volatile int *>(sh.rf[1] + JB_W);
+    sh.own_la = reinterpret_cast<volatile unsigned *>(sh.rf[1] + JB_W + 1);
+    sh.own_io = sh.own_la + 1;
     for (int i = threadIdx.x; i < d; i += JB_NT) sh.dg[i] = __ldcg(a.dg + i);
-    if (threadIdx.x == 0) *sh.cnt = 0;
+    if (threadIdx.x == 0) {
+        *sh.cnt = 0;
+        *sh.own_la = 0u;
+        *sh.own_io = 0u;
+    }
     __syncthreads();
     unsigned seq = 1, start = 1, prev_start = 0;
     int prev_nw = 0;
@@ -331,13 +371,18 @@ __device__ void jb_chain_cta(const JbArgs &a, double *smem) {
                 // release the chain first when this window's block is already loaded; the
                 // previous window's buffers (other parity) are written back meanwhile
                 if (!deferred) asm volatile("bar.sync 2, 96;" ::: "memory");
+                JB_T0(tp);
                 if (pp >= 0) jb_publish(a, sh, pp, pm, pnw, seq - 1, io_t);
+                if (io_t == 0) JB_ACC(4, tp);
                 if (deferred) {
-                    if (warp == 2) jb_wait_owners(a, jb_need_diag(m, prev_start, prev_nw));
+                    JB_T0(td);
+                    if (warp == 2) jb_wait_owners(a, jb_need_diag(m, prev_start, prev_nw), sh.own_io);
                     asm volatile("bar.sync 3, 64;" ::: "memory");
                     jb_load_diag(a, sh.B[seq & 1], p, m, io_t);
+                    if (io_t == 0) JB_ACC(5, td);
                     asm volatile("bar.sync 2, 96;" ::: "memory");
                 }
+                JB_T0(tf);
                 // prefetch the next window's diagonal block when its sources are final
                 int np = p, nm = m + 1;
                 unsigned need;
@@ -349,21 +394,37 @@ __device__ void jb_chain_cta(const JbArgs &a, double *smem) {
                     need = jb_need_diag(0, start, nw);
                 }
                 if (np < d - 1 && need <= seq - 1) {
-                    if (warp == 2) jb_wait_owners(a, need);
+                    if (warp == 2) jb_wait_owners(a, need, sh.own_io);
                     asm volatile("bar.sync 3, 64;" ::: "memory");
                     jb_load_diag(a, sh.B[(seq + 1) & 1], np, nm, io_t);
                     deferred = false;
                 } else {
                     deferred = true;
                 }
+                if (io_t == 0) JB_ACC(6, tf);
             } else if (warp == 0) {
+                JB_T0(tb);
                 asm volatile("bar.sync 2, 96;" ::: "memory");
+                if (threadIdx.x == 0) JB_ACC(1, tb);
+                JB_T0(tc);
                 jb_chain_window(a, sh, p, m, seq, app);
+                __syncwarp();
+                asm volatile("bar.sync 4, 64;" ::: "memory");  // hand the ring to the lookahead
                 if (m == nw - 1 && threadIdx.x == 0) sh.dg[p] = app;
+                if (threadIdx.x == 0) JB_ACC(0, tc);
             } else {
+                JB_T0(tl);
                 jb_lookahead(a, sh, p, m, seq, start, prev_start, prev_nw);
+                if (threadIdx.x == 32) JB_ACC(2, tl);
             }
+            JB_T0(te);
             __syncthreads();
+            if (threadIdx.x == 0) {
+                JB_ACC(7, te);
+#ifdef SGP_JBIG_PROF
+                atomicAdd(&jb_prof[8], 1ull);
+#endif
+            }
             pp = p;
             pm = m;
             pnw = nw;
@@ -387,15 +448,30 @@ __device__ void jb_owner_cta(const JbArgs &a, double *smem) {
     double *rc = smem, *rs = smem + JB_W;
     int *rf = reinterpret_cast<int *>(smem + 2 * JB_W);
     int *anyrot = rf + JB_W;
+    volatile unsigned *pub_cache = reinterpret_cast<volatile unsigned *>(anyrot + 1);
+    volatile unsigned *own_cache = pub_cache + 1;
+    if (threadIdx.x == 0) {
+        *pub_cache = 0u;
+        *own_cache = 0u;
+    }
+    __syncthreads();
     unsigned seq = 1;
     for (int p = 0; p < d - 1; ++p) {
         const int nw = jb_nw(d, p);
+        const unsigned start = seq;
         for (int m = 0; m < nw; ++m, ++seq) {
             const int q0 = p + 1 + JB_W * m, n = min(JB_W, d - q0);
             const bool last = m == nw - 1;
-            if (threadIdx.x == 0)
-                while (jb_ld_acquire(a.pub) < seq) __nanosleep(32);
-            if (threadIdx.x < 32) jb_wait_owners(a, seq - 1);
+            if (threadIdx.x == 0 && *pub_cache < seq) {
+                unsigned v;
+                while ((v = jb_ld_acquire(a.pub)) < seq) __nanosleep(32);
+                *pub_cache = v;
+            }
+            // What this window reads was last written (a) by any owner anywhere in pass p-1,
+            // or (b) in pass p by the chain CTA (covered by pub >= seq) or by an owner at the
+            // window of the element's earlier index, three or more windows back.  So: every
+            // owner past pass p-1 for the first three windows of a pass, else past seq - 3.
+            if (threadIdx.x < 32) jb_wait_owners(a, m >= 3 ? seq - 3 : start - 1, own_cache);
             __syncthreads();
             if (threadIdx.x < 32) {
                 const int j = threadIdx.x;
@@ -473,7 +549,7 @@ __global__ void __launch_bounds__(JB_NT) k_jb_sweep(JbArgs a) {
 
 static size_t jb_smem_bytes(int d) {
     return sizeof(double) * ((size_t)((d + 1) & ~1) + 2 * (JB_W * JB_LDB + 1) + 4 * JB_W + 3 * JB_W) +
-           sizeof(int) * (2 * JB_W + 4);
+           sizeof(int) * (2 * JB_W + 8);
 }
 
 // Eigenvector update (_jacobi.py:81-85) on Vt = V^T: element (k, p) of V is Vt[p][k].  Thread
@@ -685,10 +761,32 @@ static int jb_jacobi(JbWS &w, double *A, double *V, int d, double tol, double sk
         a.nown = w.nown;
         a.skip = skip;
         void *args[] = {&a};
+        static const bool dbg = getenv("SGP_DEBUG_JBIG") != nullptr;
+        cudaEvent_t t0 = nullptr, t1 = nullptr;
+        if (dbg) {
+            cudaEventCreate(&t0);
+            cudaEventCreate(&t1);
+            cudaEventRecord(t0, s);
+        }
         if (cudaLaunchCooperativeKernel((const void *)k_jb_sweep, dim3(1 + w.nown), dim3(JB_NT), args, w.smem, s) !=
             cudaSuccess) {
             rc = -2;
             break;
+        }
+        if (dbg) {  // diagnostics: sweep time against rotations applied
+            cudaEventRecord(t1, s);
+            cudaEventSynchronize(t1);
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, t0, t1);
+            const size_t E = (size_t)d * (d - 1) / 2;
+            std::vector<int> f(E);
+            cudaMemcpy(f.data(), w.logf[b], sizeof(int) * E, cudaMemcpyDeviceToHost);
+            long nrot = 0;
+            for (int v : f) nrot += v;
+            fprintf(stderr, "jbig d=%d sweep %d: %.1f ms, %ld of %zu rotations (%.3f us/rotation)\n", d, sw, ms, nrot, E,
+                    nrot ? 1e3 * ms / nrot : 0.0);
+            cudaEventDestroy(t0);
+            cudaEventDestroy(t1);
         }
         cudaEventRecord(w.evA[b], s);
         cudaStreamWaitEvent(w.s2, w.evA[b], 0);
