@@ -69,6 +69,8 @@ extern "C" {
 #define SGP_ORDER_PARALLEL 1        /* round-robin (Brent-Luk) order: d/2 rotations per round */
 #define SGP_ORDER_REFINE 2          /* warm only, d > 256: GEMM eigenvector refinement (Ogita-Aishima),
                                        block-Jacobi fallback; elsewhere treated as PARALLEL */
+#define SGP_ORDER_DC 3              /* cold only, large-d path: Householder tridiagonalisation +
+                                       divide and conquer (sgp_eigh_dc); eigenvalues ascending */
 
 /* what sgp_eval computes */
 #define SGP_EVAL_POTENTIAL 1
@@ -193,6 +195,11 @@ int sgp_potential_derivatives(int likelihood, int n, int J, const double *d_f,
  * bit-compatible with _jacobi.jacobi_sweeps.  d_sweeps = -1 on cap. */
 int sgp_eigh_cold(int Z, int d, const double *d_h, double zeta, int sweep_cap,
                   double *d_lam, double *d_psi, int *d_sweeps, void *stream);
+/* Symmetric eigendecomposition of 0.5 (H + H^T) by blocked Householder tridiagonalisation +
+ * divide and conquer (north star (3)): lam ascending, psi[i*d + k] = component i of
+ * eigenvector k.  Not order-exact with the reference's Jacobi (static_eigendecompose,
+ * metric.py:112-127, up to eigenpair order and signs).  1 <= d <= 4096. */
+int sgp_eigh_dc(int Z, int d, const double *d_h, double *d_lam, double *d_psi, void *stream);
 /* Warm decomposition in the previous basis (dynamic_eigendecompose). */
 int sgp_eigh_warm(int Z, int d, const double *d_h, const double *d_psi_prev,
                   const int *d_since_prev, int gs_interval, double zeta, int sweep_cap,

@@ -36,7 +36,7 @@ TRANSFORM_LOG = 0
 TRANSFORM_IDENTITY = 1
 
 METRIC_CODES = {"softabs-dynamic": 0, "softabs-static": 1, "euclidean": 2}
-ORDER_CODES = {"cyclic": 0, "parallel": 1, "refine": 2}
+ORDER_CODES = {"cyclic": 0, "parallel": 1, "refine": 2, "dc": 3}
 PATH_CODES = {"auto": 0, "latency": 1}
 
 EVAL_POTENTIAL = 1
@@ -145,6 +145,7 @@ def lib():
         "sgp_trace": (i, [vp, i, vp, vp, vp, vp, vp, vp, vp]),
         "sgp_potential_derivatives": (i, [i, i, i, vp, vp, d, vp, vp, vp, vp, vp]),
         "sgp_eigh_cold": (i, [i, i, vp, d, i, vp, vp, vp, vp]),
+        "sgp_eigh_dc": (i, [i, i, vp, vp, vp, vp]),
         "sgp_eigh_warm": (i, [i, i, vp, vp, vp, i, d, i, i, vp, vp, vp, vp, vp]),
         "sgp_mgs": (i, [i, i, vp, vp]),
         "sgp_t_matrix": (i, [i, i, vp, d, vp, vp]),

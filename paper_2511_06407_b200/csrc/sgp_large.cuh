@@ -18,6 +18,7 @@
 #include "sgp_chain.cuh"
 #include "sgp_gemm.cuh"
 #include "sgp_jbig.cuh"
+#include "sgp_dc.cuh"
 
 #define LG_NT 256
 
@@ -39,6 +40,8 @@ struct LgPtrs {
     cudaEvent_t bj_ev[5];
     // reference-order Jacobi (sgp_jbig.cuh) workspace, allocated on first use
     JbWS *jb;
+    // tridiagonalisation + divide and conquer workspace (cold_order="dc"), allocated on first use
+    DcWS *dc;
 };
 
 static void lg_free_handles(LgPtrs &L) {
@@ -46,6 +49,11 @@ static void lg_free_handles(LgPtrs &L) {
         jb_ws_free(*L.jb);
         delete L.jb;
         L.jb = nullptr;
+    }
+    if (L.dc) {
+        dc_ws_free(*L.dc);
+        delete L.dc;
+        L.dc = nullptr;
     }
     if (L.bj_hs) cudaStreamDestroy(L.bj_hs);
     for (cudaEvent_t &e : L.bj_ev)
@@ -1194,8 +1202,23 @@ static int lg_jacobi(LgCtx &c, int dst, double tol, double skip, bool parallel, 
 }
 
 // cold decomposition of H into slot dst (metric.py:112-142)
+__global__ void k_lg_set_diag(double *H, const double *lam, int d) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < d; i += gridDim.x * blockDim.x)
+        H[(size_t)i * d + i] = lam[i];
+}
+
 static int lg_eig_cold(LgCtx &c, int dst, int *sweeps) {
     const int d = c.d;
+    if (c.cfg.cold_order == SGP_ORDER_DC && c.L.dc && d <= DC_NMAX) {
+        // tridiagonalisation + divide and conquer (sgp_dc.cuh); symmetrises H itself
+        double *lam = c.L.vec + (size_t)V_TMP * d;
+        if (dc_eigh(*c.L.dc, c.L.H, d, d, lam, c.L.P[dst], d, c.s)) return SGP_STATUS_JACOBI;
+        k_lg_set_diag<<<lg_blocks(d), 256, 0, c.s>>>(c.L.H, lam, d);
+        *sweeps = 0;
+        lg_op(c, LG_GLAM, dst, 0, 0, 0);
+        c.since[dst] = 0;
+        return lg_sync(c);
+    }
     k_lg_symmetrize<<<lg_blocks((size_t)d * d), 256, 0, c.s>>>(c.L.H, d);
     const double hnorm = lg_hnorm(c);
     const double tol = c.cfg.zeta * hnorm, skip = d ? tol / d : 0.0;
@@ -1777,6 +1800,7 @@ static int lg_alloc(const ModelDev &M, LgPtrs &L, void **owner) {
         }
     }
     L.jb = new JbWS();
+    L.dc = new DcWS();
     *owner = base;
     return SGP_OK;
 }

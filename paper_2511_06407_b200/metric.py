@@ -117,6 +117,24 @@ def static_eigendecompose(hessian, zeta, sweep_cap=DEFAULT_SWEEP_CAP):
     return lam, psi, int(sw[0])
 
 
+def eigh_dc(hessian):
+    """Eigendecomposition of the symmetric part of ``hessian`` by blocked Householder
+    tridiagonalisation + divide and conquer on the device (sgp_dc.cuh; north star (3)).
+
+    Returns (eigenvalues ascending, eigenvectors as columns).  The fast cold decomposition for
+    latent-function-sized d; unlike static_eigendecompose it does not follow the reference's
+    Jacobi order (metric.py:112-127), only its result up to eigenpair order and signs."""
+    h = np.asarray(hessian, dtype=float)
+    if h.ndim != 2 or h.shape[0] != h.shape[1]:
+        raise ValueError("hessian must be square")
+    L = nat.lib()
+    d = h.shape[0]
+    th = nat.dev_f64(h)
+    lam, psi = nat.empty_f64(d), nat.empty_f64(d, d)
+    nat.check(L.sgp_eigh_dc(1, d, nat.ptr(th), nat.ptr(lam), nat.ptr(psi), nat.stream()), "sgp_eigh_dc")
+    return _sync_numpy(lam, psi)
+
+
 def metric_from_hessian(hessian, kappa, zeta, sweep_cap=DEFAULT_SWEEP_CAP):
     """MetricState from a cold decomposition (metric.py:130-142)."""
     lam, psi, sweeps = static_eigendecompose(hessian, zeta, sweep_cap)

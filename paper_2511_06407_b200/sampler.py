@@ -26,7 +26,7 @@ from .posterior import DivergenceError, DomainError, PosteriorTarget, raise_stat
 LN_2PI = math.log(2.0 * math.pi)
 METRIC_MODES = ("softabs-dynamic", "softabs-static", "euclidean")
 WARM_ORDERS = ("parallel", "cyclic", "refine")
-COLD_ORDERS = ("parallel", "cyclic")
+COLD_ORDERS = ("parallel", "cyclic", "dc")
 _DIVERGENT = (DivergenceError, DomainError, JacobiError, FloatingPointError)
 
 

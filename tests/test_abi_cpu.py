@@ -49,6 +49,8 @@ def test_null_arguments_are_rejected_without_gpu(lib):
     assert lib.sgp_eval(None, 1, None, None, 0, None, None, None, None, None, None, None) == -1
     assert lib.sgp_run_moves(None, None, None, 1, 0, None, None, None, None) == -1
     assert lib.sgp_eigh_cold(0, 3, None, ctypes.c_double(1e-13), 30, None, None, None, None) == -1
+    assert lib.sgp_eigh_dc(1, 0, None, None, None, None) == -1
+    assert lib.sgp_eigh_dc(1, 5000, None, None, None, None) == -1
 
 
 def test_library_built_for_sm100a():
