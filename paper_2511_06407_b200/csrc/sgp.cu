@@ -534,13 +534,22 @@ static int eigh_cold_big(int Z, int d, const double *d_h, double zeta, int cap, 
 
 extern "C" int sgp_eigh_dc(int Z, int d, const double *d_h, double *d_lam, double *d_psi, void *stream) {
     if (Z < 1 || d < 1 || d > DC_NMAX || !d_h || !d_lam || !d_psi) return SGP_EINVAL;
-    DcWS w;
+    // one workspace per host thread and device, kept between calls (re-allocated when d changes)
+    struct Cache {
+        DcWS w[16];
+        ~Cache() {
+            for (DcWS &x : w) dc_ws_free(x);
+        }
+    };
+    static thread_local Cache cache;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    DcWS &w = cache.w[dev & 15];
     int rc = SGP_OK;
     const size_t dd = (size_t)d * d;
     for (int z = 0; z < Z && rc == SGP_OK; ++z)
         if (dc_eigh(w, d_h + z * dd, d, d, d_lam + (size_t)z * d, d_psi + z * dd, d, S(stream))) rc = SGP_ECUDA;
     if (cudaStreamSynchronize(S(stream)) != cudaSuccess) rc = SGP_ECUDA;
-    dc_ws_free(w);
     return rc;
 }
 

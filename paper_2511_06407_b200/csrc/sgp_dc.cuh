@@ -39,10 +39,11 @@
 
 #define DC_NB 32     // reflectors per panel
 #define DC_PT 512    // threads of the panel kernel
-#define DC_PS 72     // per-CTA partial stride (doubles): [0] |x|^2, [1..32] W^T v, [33..64] V^T v, [65] w^T v
+#define DC_PS 72     // per-CTA partial stride (doubles): [0] |x|^2, [1..32] W^T v, [33..64] V^T v, [65] v^T y, [66] y(c+1)
 #define DC_LEAF 48   // max leaf size
 #define DC_MT 1024   // threads of the deflation kernel
 #define DC_NMAX 4096 // largest d (one merge is sorted in shared memory)
+#define DC_BT 128    // reflectors per back-transformation block
 
 __device__ __forceinline__ unsigned dc_ld_acquire(const unsigned *p) {
     unsigned v;
@@ -78,6 +79,23 @@ __device__ __forceinline__ double dc_warp_parts(const double *part, int t, int n
     return dc_warp_sum(s);
 }
 
+#ifdef SGP_DC_PROF_CYC
+#ifndef DC_PROF_BLK
+#define DC_PROF_BLK 0
+#endif
+// cycles of CTA 0 per panel-kernel phase, summed over columns (tools/dc_prof.cu)
+__device__ unsigned long long dc_prof[8];
+#define DC_T0(v) long long v = clock64()
+#define DC_ACC(i, v)                                                                \
+    do {                                                                            \
+        if (blockIdx.x == DC_PROF_BLK && threadIdx.x == 0) dc_prof[i] += clock64() - (v); \
+        v = clock64();                                                              \
+    } while (0)
+#else
+#define DC_T0(v)
+#define DC_ACC(i, v)
+#endif
+
 // ---------------------------------------------------------------------------
 // stage 1: one panel of the tridiagonalisation
 
@@ -85,48 +103,80 @@ struct DcPanel {
     double *A;  // n x ld, full symmetric; row c receives the updated column c
     int ld, n, k0, nbp;
     double *V;  // n x ld: V[r*ld + c] = v_c(r) (zero for r <= c, 1 at r = c+1)
-    double *W;  // n x DC_NB
+    double *W;  // n x ld (first DC_NB columns): the panel's W
     double *y, *wt;            // [n] scratch
     double *dv, *ev, *tau;     // tridiagonal diagonal, off-diagonal, reflector scalars
     double *part;              // [grid][DC_PS]
     unsigned *bar;
 };
 
+// rows a warp owns (row r -> warp r mod warps): n <= DC_RPW * warps
+#define DC_RPW 2
+// most CTAs of the cooperative panel kernel (partials reduced with all loads in flight)
+#define DC_MAXG 160
+
+// symmetric mat-vec of one row segment against v (smem), 16 loads in flight per lane.  Plain
+// (L1-allocating) loads: a warp re-reads its own rows every column, and a row is never written
+// while it is inside the mat-vec range (row c+1 is rewritten only after its last mat-vec).
+__device__ __forceinline__ double dc_ld_l1(const double *p) {
+    double v;
+    asm volatile("ld.global.ca.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ double dc_row_dot(const double *row, const double *v, int m) {
+    const int lane = threadIdx.x & 31;
+    double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
+    double buf[8], nxt[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+        const int i = lane + 32 * u;
+        buf[u] = i < m ? dc_ld_l1(row + i) : 0.0;
+    }
+    for (int base = 0; base < m; base += 256) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int i = base + 256 + lane + 32 * u;
+            nxt[u] = i < m ? dc_ld_l1(row + i) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int i = base + lane + 32 * u;
+            const double vi = i < m ? v[i] : 0.0;
+            if (u & 1) {
+                if (u & 2) acc3 = __fma_rn(buf[u], vi, acc3);
+                else acc1 = __fma_rn(buf[u], vi, acc1);
+            } else {
+                if (u & 2) acc2 = __fma_rn(buf[u], vi, acc2);
+                else acc0 = __fma_rn(buf[u], vi, acc0);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) buf[u] = nxt[u];
+    }
+    return dc_warp_sum((acc0 + acc1) + (acc2 + acc3));
+}
+
+// Per column c (panel index j) with two grid barriers:
+//   P  reflector of column c (its update is already in row c): ||x||^2 from the partials,
+//      v staged in shared memory
+//   S  y = A22 v on the owned rows, partials of W^T v, V^T v and v^T y          -> barrier A
+//   W  s = w^T v = tau (v^T y - 2 (W^T v).(V^T v)) (no third reduction), w = tau (y - V W^T v
+//      - W V^T v) - tau/2 s v stored as W(:, j), then column c+1 minus the rank-2(j+1)
+//      correction into row c+1 with its ||x||^2 partial                          -> barrier B
 __global__ void __launch_bounds__(DC_PT, 1) k_dc_panel(DcPanel a) {
     extern __shared__ double vs[];  // v of the current column, rows c+1..n-1
-    __shared__ double red[DC_PT / 32][2 * DC_NB];
-    __shared__ double u[2 * DC_NB];  // W^T v, V^T v (all CTAs)
-    __shared__ double sc[4];
     constexpr int NW = DC_PT / 32;
+    __shared__ double red[NW][2 * DC_NB + 2];
+    __shared__ double u[2 * DC_NB + 2];  // u1 = W^T v [0, j), u2 = V^T v [j, 2j), v^T y [2j], y(c+1) [2j+1]
+    __shared__ double rowv[DC_NB + 1], roww[DC_NB + 1];  // V(c+1, :), W(c+1, :)
+    __shared__ double sc[4];
     const int n = a.n, ld = a.ld, k0 = a.k0;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int gw = blockIdx.x * NW + warp, NWG = gridDim.x * NW;
     unsigned target = 0;
-    double wrow = 0.0;  // W(c, j-1), computed by every CTA at the end of column c-1
-    for (int j = 0; j < a.nbp; ++j) {
-        const int c = k0 + j, m = n - c - 1;
-        // ---- (1) column c minus the rank-2j panel correction, stored into row c
-        double vci = 0.0, wci = 0.0;
-        if (lane < j) {
-            vci = lane == j - 1 ? 1.0 : __ldcg(a.V + (size_t)c * ld + k0 + lane);
-            wci = lane == j - 1 ? wrow : __ldcg(a.W + (size_t)c * DC_NB + lane);
-        }
-        double sq = 0.0;
-        for (int r = c + (gw - c % NWG + NWG) % NWG; r < n; r += NWG) {
-            double t = 0.0;
-            if (lane < j) {
-                const double vri = r == c ? vci : __ldcg(a.V + (size_t)r * ld + k0 + lane);
-                const double wri = r == c ? wci : __ldcg(a.W + (size_t)r * DC_NB + lane);
-                t = __fma_rn(vri, wci, __dmul_rn(wri, vci));
-            }
-            t = dc_warp_sum(t);
-            if (lane == 0) {
-                const double arc = __ldcg(a.A + (size_t)r * ld + c) - t;
-                a.A[(size_t)c * ld + r] = arc;
-                if (r == c) a.dv[c] = arc;
-                if (r >= c + 2) sq = __fma_rn(arc, arc, sq);
-            }
-        }
+    auto first_row = [&](int lo) { return lo + (gw - lo % NWG + NWG) % NWG; };
+    auto put_sq = [&](double sq) {  // ||x||^2 partial of this CTA -> part[b][0]
+        sq = dc_warp_sum(sq);
         if (lane == 0) red[warp][0] = sq;
         __syncthreads();
         if (warp == 0) {
@@ -134,12 +184,37 @@ __global__ void __launch_bounds__(DC_PT, 1) k_dc_panel(DcPanel a) {
             v = dc_warp_sum(v);
             if (lane == 0) a.part[(size_t)blockIdx.x * DC_PS] = v;
         }
+    };
+    {  // prologue: column k0 needs no panel correction
+        DC_T0(tp);
+        double sq = 0.0;
+        for (int r = first_row(k0); r < n; r += NWG) {
+            if (lane == 0) {
+                const double arc = __ldcg(a.A + (size_t)r * ld + k0);
+                a.A[(size_t)k0 * ld + r] = arc;
+                if (r == k0) a.dv[k0] = arc;
+                if (r >= k0 + 2) sq = __fma_rn(arc, arc, sq);
+            }
+        }
+        put_sq(sq);
+        DC_ACC(0, tp);
         dc_grid_sync(a.bar, target);
-        // ---- (2) the reflector H = I - tau v v^T with H x = beta e1 (dlarfg), in every CTA
+        DC_ACC(1, tp);
+    }
+    for (int j = 0; j < a.nbp; ++j) {
+        const int c = k0 + j, m = n - c - 1;
+        DC_T0(tp);
+        // ---- P: the reflector H = I - tau v v^T with H x = beta e1 (dlarfg), in every CTA
+        double raw[(DC_NMAX + DC_PT - 1) / DC_PT];
+#pragma unroll
+        for (int q = 0; q < (DC_NMAX + DC_PT - 1) / DC_PT; ++q) {
+            const int i = threadIdx.x + q * DC_PT;
+            raw[q] = i < m ? __ldcg(a.A + (size_t)c * ld + c + 1 + i) : 0.0;
+        }
         if (warp == 0) {
             const double xn2 = dc_warp_parts(a.part, 0, gridDim.x);
             if (lane == 0) {
-                const double alpha = m > 0 ? __ldcg(a.A + (size_t)c * ld + c + 1) : 0.0;
+                const double alpha = raw[0];
                 double tau = 0.0, scal = 0.0, beta = alpha;
                 if (xn2 > 0.0) {
                     beta = -copysign(sqrt(__fma_rn(alpha, alpha, xn2)), alpha);
@@ -156,101 +231,139 @@ __global__ void __launch_bounds__(DC_PT, 1) k_dc_panel(DcPanel a) {
         }
         __syncthreads();
         const double tau = sc[0], scal = sc[1];
-        for (int i = threadIdx.x; i < m; i += DC_PT)
-            vs[i] = i == 0 ? 1.0 : __ldcg(a.A + (size_t)c * ld + c + 1 + i) * scal;
+#pragma unroll
+        for (int q = 0; q < (DC_NMAX + DC_PT - 1) / DC_PT; ++q) {
+            const int i = threadIdx.x + q * DC_PT;
+            if (i < m) vs[i] = i == 0 ? 1.0 : raw[q] * scal;
+        }
         __syncthreads();
-        // ---- (3) y = A22 v over the rows this warp owns, and the panel dot products
-        double acc1 = 0.0, acc2 = 0.0;  // lane i < j: sum_r W(r,i) v(r), sum_r V(r,i) v(r)
-        for (int r = c + 1 + (gw - (c + 1) % NWG + NWG) % NWG; r < n; r += NWG) {
-            const double *row = a.A + (size_t)r * ld + c + 1;
-            double y0 = 0.0, y1 = 0.0, y2 = 0.0, y3 = 0.0;
-            int i = lane;
-            for (; i + 96 < m; i += 128) {
-                const double a0 = __ldcg(row + i), a1 = __ldcg(row + i + 32), a2 = __ldcg(row + i + 64),
-                             a3 = __ldcg(row + i + 96);
-                y0 = __fma_rn(a0, vs[i], y0);
-                y1 = __fma_rn(a1, vs[i + 32], y1);
-                y2 = __fma_rn(a2, vs[i + 64], y2);
-                y3 = __fma_rn(a3, vs[i + 96], y3);
-            }
-            for (; i < m; i += 32) y0 = __fma_rn(__ldcg(row + i), vs[i], y0);
-            const double yr = dc_warp_sum((y0 + y1) + (y2 + y3));
-            if (lane == 0) a.y[r] = yr;
-            if (lane < j) {
-                const double vr = vs[r - c - 1];
-                acc1 = __fma_rn(__ldcg(a.W + (size_t)r * DC_NB + lane), vr, acc1);
-                acc2 = __fma_rn(__ldcg(a.V + (size_t)r * ld + k0 + lane), vr, acc2);
+        DC_ACC(2, tp);
+        // ---- S: y = A22 v on the owned rows; partial dot products; prefetch for W
+        double yq[DC_RPW], vq[DC_RPW], vr[DC_RPW], wr[DC_RPW], an[DC_RPW];
+        double acc1 = 0.0, acc2 = 0.0, yv = 0.0;
+        {
+            const int r0 = first_row(c + 1);
+#pragma unroll
+            for (int q = 0; q < DC_RPW; ++q) {
+                const int r = r0 + q * NWG;
+                if (r >= n) break;
+                vr[q] = lane < j ? __ldcg(a.V + (size_t)r * ld + k0 + lane) : 0.0;
+                wr[q] = lane < j ? __ldcg(a.W + (size_t)r * ld + lane) : 0.0;
+                an[q] = (j + 1 < a.nbp && lane == 0) ? __ldcg(a.A + (size_t)r * ld + c + 1) : 0.0;
+                const double yr = dc_row_dot(a.A + (size_t)r * ld + c + 1, vs, m);
+                const double vv = vs[r - c - 1];
+                yq[q] = yr;
+                vq[q] = vv;
+                if (lane == 0) {
+                    a.y[r] = yr;
+                    yv = __fma_rn(yr, vv, yv);
+                }
+                acc1 = __fma_rn(wr[q], vv, acc1);
+                acc2 = __fma_rn(vr[q], vv, acc2);
             }
         }
         red[warp][lane] = acc1;
         red[warp][DC_NB + lane] = acc2;
+        if (lane == 0) {
+            red[warp][2 * DC_NB] = yv;
+            red[warp][2 * DC_NB + 1] = (first_row(c + 1) == c + 1 && m > 0) ? yq[0] : 0.0;  // y(c+1) owner
+        }
         __syncthreads();
-        if (threadIdx.x < 2 * DC_NB) {
+        if (threadIdx.x < 2 * DC_NB + 2) {
             double v = 0.0;
             for (int w = 0; w < NW; ++w) v += red[w][threadIdx.x];
             a.part[(size_t)blockIdx.x * DC_PS + 1 + threadIdx.x] = v;
         }
+        DC_ACC(3, tp);
         dc_grid_sync(a.bar, target);
-        // ---- (4) w = tau (y - V (W^T v) - W (V^T v)) and the partial w^T v
-        for (int t = warp; t < 2 * j; t += NW) {
-            const int idx = t < j ? t : DC_NB + (t - j);
-            const double s = dc_warp_parts(a.part, 1 + idx, gridDim.x);
-            if (lane == 0) u[idx] = s;
-        }
-        __syncthreads();
-        double sp = 0.0;
-        for (int r = c + 1 + (gw - (c + 1) % NWG + NWG) % NWG; r < n; r += NWG) {
-            double t = 0.0;
-            if (lane < j)
-                t = __fma_rn(__ldcg(a.V + (size_t)r * ld + k0 + lane), u[lane],
-                             __dmul_rn(__ldcg(a.W + (size_t)r * DC_NB + lane), u[DC_NB + lane]));
-            t = dc_warp_sum(t);
-            if (lane == 0) {
-                const double w = tau * (__ldcg(a.y + r) - t);
-                a.wt[r] = w;
-                sp = __fma_rn(w, vs[r - c - 1], sp);
+        DC_ACC(1, tp);
+        // ---- W: the reductions, 4 lanes per value (same order in every CTA)
+        {
+            // value g: u1 [0, j), u2 [j, 2j), v^T y (2j), y(c+1) (2j+1); 8 lanes per value
+            const int g = threadIdx.x >> 3, sub = threadIdx.x & 7;
+            const int idx = g < j ? 1 + g : (g < 2 * j ? 1 + DC_NB + (g - j) : 1 + 2 * DC_NB + (g - 2 * j));
+            constexpr int MAXB = (DC_MAXG + 7) / 8;
+            double pv[MAXB];
+#pragma unroll
+            for (int t = 0; t < MAXB; ++t) {
+                const int b = sub + 8 * t;
+                pv[t] = (g <= 2 * j + 1 && b < (int)gridDim.x) ? __ldcg(a.part + (size_t)b * DC_PS + idx) : 0.0;
+            }
+            double sm = 0.0;
+#pragma unroll
+            for (int t = 0; t < MAXB; ++t) sm += pv[t];
+            sm += __shfl_xor_sync(0xffffffffu, sm, 1);
+            sm += __shfl_xor_sync(0xffffffffu, sm, 2);
+            sm += __shfl_xor_sync(0xffffffffu, sm, 4);
+            if (sub == 0 && g <= 2 * j + 1) u[g] = sm;
+            if (warp == 1 && lane < j) {
+                rowv[lane] = __ldcg(a.V + (size_t)(c + 1) * ld + k0 + lane);
+                roww[lane] = __ldcg(a.W + (size_t)(c + 1) * ld + lane);
             }
         }
-        if (lane == 0) red[warp][0] = sp;
         __syncthreads();
         if (warp == 0) {
-            double v = lane < NW ? red[lane][0] : 0.0;
-            v = dc_warp_sum(v);
-            if (lane == 0) a.part[(size_t)blockIdx.x * DC_PS + 1 + 2 * DC_NB] = v;
-        }
-        dc_grid_sync(a.bar, target);
-        // ---- (5) w -= tau/2 (w^T v) v; V(:, c) = v
-        if (warp == 0) {
-            const double s = dc_warp_parts(a.part, 1 + 2 * DC_NB, gridDim.x);
-            if (lane == 0) sc[2] = -0.5 * tau * s;
-        }
-        __syncthreads();
-        const double alpha2 = sc[2];
-        for (int r = c + 2 + (gw - (c + 2) % NWG + NWG) % NWG; r < n; r += NWG) {
-            if (lane == 0) {
-                const double vr = vs[r - c - 1];
-                a.W[(size_t)r * DC_NB + j] = __fma_rn(alpha2, vr, __ldcg(a.wt + r));
-                a.V[(size_t)r * ld + c] = vr;
-            }
-        }
-        // row c+1 (needed by every CTA in the next column): recomputed identically everywhere
-        if (warp == 0 && m > 0) {
-            double t = 0.0;
-            if (lane < j)
-                t = __fma_rn(__ldcg(a.V + (size_t)(c + 1) * ld + k0 + lane), u[lane],
-                             __dmul_rn(__ldcg(a.W + (size_t)(c + 1) * DC_NB + lane), u[DC_NB + lane]));
+            // alpha2 = -tau/2 w^T v with w^T v = tau (v^T y - 2 u1.u2)
+            double t = lane < j ? u[lane] * u[j + lane] : 0.0;
             t = dc_warp_sum(t);
+            const double s = tau * (u[2 * j] - 2.0 * t);
+            const double alpha2 = -0.5 * tau * s;
+            // W(c+1, j): row c+1 recomputed identically in every CTA
+            double t2 = 0.0;
+            if (m > 0 && lane < j) t2 = __fma_rn(rowv[lane], u[lane], __dmul_rn(roww[lane], u[j + lane]));
+            t2 = dc_warp_sum(t2);
             if (lane == 0) {
-                const double w = alpha2 + tau * (__ldcg(a.y + c + 1) - t);
-                sc[3] = w;
-                if (blockIdx.x == 0) {
-                    a.W[(size_t)(c + 1) * DC_NB + j] = w;
+                sc[2] = alpha2;
+                const double w1 = m > 0 ? alpha2 + tau * (u[2 * j + 1] - t2) : 0.0;
+                sc[3] = w1;
+                if (blockIdx.x == 0 && m > 0) {
+                    a.W[(size_t)(c + 1) * ld + j] = w1;
                     a.V[(size_t)(c + 1) * ld + c] = 1.0;
                 }
             }
         }
         __syncthreads();
-        wrow = sc[3];
+        const double alpha2 = sc[2], wrow = sc[3];
+        const bool next = j + 1 < a.nbp;
+        // V(c+1, i) and W(c+1, i) for i <= j, as the next column's update needs them
+        const double v1 = lane < j ? rowv[lane] : (lane == j ? 1.0 : 0.0);
+        const double w1 = lane < j ? roww[lane] : (lane == j ? wrow : 0.0);
+        double sq = 0.0;
+        {
+            const int r0 = first_row(c + 1);
+#pragma unroll
+            for (int q = 0; q < DC_RPW; ++q) {
+                const int r = r0 + q * NWG;
+                if (r >= n) break;
+                double t = 0.0;
+                if (lane < j) t = __fma_rn(vr[q], u[lane], __dmul_rn(wr[q], u[j + lane]));
+                t = dc_warp_sum(t);
+                const double w = r == c + 1 ? wrow : __fma_rn(alpha2, vq[q], tau * (yq[q] - t));
+                if (lane == 0 && r >= c + 2) {
+                    a.W[(size_t)r * ld + j] = w;
+                    a.V[(size_t)r * ld + c] = vq[q];
+                }
+                if (next) {  // column c+1 of row r minus sum_{i<=j} V(r,i) W(c+1,i) + W(r,i) V(c+1,i)
+                    const double vri = lane == j ? vq[q] : vr[q], wri = lane == j ? w : wr[q];
+                    double cr = lane <= j ? __fma_rn(vri, w1, __dmul_rn(wri, v1)) : 0.0;
+                    cr = dc_warp_sum(cr);
+                    if (lane == 0) {
+                        const double arc = an[q] - cr;
+                        a.A[(size_t)(c + 1) * ld + r] = arc;
+                        if (r == c + 1) a.dv[c + 1] = arc;
+                        if (r >= c + 3) sq = __fma_rn(arc, arc, sq);
+                    }
+                }
+            }
+        }
+        if (next) {
+            put_sq(sq);
+            DC_ACC(4, tp);
+            dc_grid_sync(a.bar, target);
+            DC_ACC(1, tp);
+        } else {
+            DC_ACC(4, tp);
+        }
     }
 }
 
@@ -659,39 +772,29 @@ __global__ void __launch_bounds__(256) k_dc_vec(const DcMerge *mg, const int *kc
 }
 
 // ---------------------------------------------------------------------------
-// stage 3: compact-WY T factors (dlarft, forward columnwise) of every panel
-__global__ void __launch_bounds__(1024) k_dc_tmat(const double *V, int ld, int n, const double *tau, double *Tm) {
-    __shared__ double G[DC_NB][DC_NB + 1], T[DC_NB][DC_NB + 1], tile[32][DC_NB + 1];
-    const int p = blockIdx.x, k0 = p * DC_NB, nbp = min(DC_NB, n - 1 - k0);
-    const int ti = threadIdx.x >> 5, tj = threadIdx.x & 31;  // (row, col) of the Gram entry
-    double acc = 0.0;
-    for (int r0 = k0 + 1; r0 < n; r0 += 32) {
-        __syncthreads();
-        {
-            const int r = r0 + ti;
-            tile[ti][tj] = (r < n && tj < nbp) ? V[(size_t)r * ld + k0 + tj] : 0.0;
-        }
-        __syncthreads();
-#pragma unroll 8
-        for (int l = 0; l < 32; ++l) acc = __fma_rn(tile[l][ti], tile[l][tj], acc);
-    }
-    G[ti][tj] = acc;
-    T[ti][tj] = 0.0;
+// stage 3: back-transformation
+
+// compact-WY T of a back-transformation block from its Gram G = V^T V (dlarft recurrence):
+// T(j,j) = tau_j, T(0:j, j) = -tau_j T(0:j, 0:j) G(0:j, j)
+__global__ void __launch_bounds__(DC_BT) k_dc_tblock(const double *Gm, const double *tau, int n, double *Tb) {
+    extern __shared__ double T[];  // DC_BT x (DC_BT + 1)
+    constexpr int LT = DC_BT + 1;
+    const int b = blockIdx.x, k0 = b * DC_BT, nbb = min(DC_BT, n - 1 - k0);
+    const double *G = Gm + (size_t)b * DC_BT * DC_BT;
+    const int i = threadIdx.x;
+    for (int l = 0; l < DC_BT; ++l) T[i * LT + l] = 0.0;
     __syncthreads();
-    for (int j = 0; j < nbp; ++j) {
-        // T(0:j, j) = -tau_j T(0:j, 0:j) G(0:j, j); T(j, j) = tau_j
-        const double tj_ = tau[k0 + j];
+    for (int j = 0; j < nbb; ++j) {
+        const double tj = tau[k0 + j];
         double v = 0.0;
-        if (threadIdx.x < j) {
-            const int i = threadIdx.x;
-            for (int l = i; l < j; ++l) v = __fma_rn(T[i][l], G[l][j], v);
-        }
+        if (i < j)
+            for (int l = i; l < j; ++l) v = __fma_rn(T[i * LT + l], G[(size_t)l * DC_BT + j], v);
         __syncthreads();
-        if (threadIdx.x < j) T[threadIdx.x][j] = -tj_ * v;
-        if (threadIdx.x == j) T[j][j] = tj_;
+        if (i < j) T[i * LT + j] = -tj * v;
+        if (i == j) T[j * LT + j] = tj;
         __syncthreads();
     }
-    Tm[(size_t)p * DC_NB * DC_NB + ti * DC_NB + tj] = (ti < nbp && tj < nbp) ? T[ti][tj] : 0.0;
+    for (int l = 0; l < DC_BT; ++l) Tb[(size_t)b * DC_BT * DC_BT + (size_t)i * DC_BT + l] = T[i * LT + l];
 }
 
 // ascending eigenvalues (bitonic, one CTA) and the permutation
@@ -743,9 +846,12 @@ __global__ void k_dc_gather(const double *Z, int ld, const int *perm, int n, dou
 // host side
 
 struct DcWS {
-    int n = 0, ld = 0, G = 0, L = 0, levels = 0;
+    int n = 0, ld = 0, nctas = 0, L = 0, levels = 0;
     double *base = nullptr;
-    double *A, *V, *W, *y, *wt, *dv, *ev, *tau, *part, *Q[2], *VT, *D, *pole, *zk, *zh, *rhov, *rot, *Tm, *X, *Y;
+    double *A, *V, *W, *y, *wt, *dv, *ev, *tau, *part, *Q[2], *VT, *D, *pole, *zk, *zh, *rhov, *rot, *X, *Y;
+    double *G, *Tb;     // back-transform blocks: Gram V_b^T V_b and the compact-WY T_b
+    GemmArgs *gdesc;    // the blocks' Gram GEMMs (one batched launch)
+    int nbt;
     int *col, *kc, *bnd, *perm;
     unsigned *bar;
     DcMerge *mg;
@@ -793,21 +899,27 @@ static inline int dc_ws_alloc(DcWS &w, int n) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const size_t psmem = sizeof(double) * (size_t)n;
     cudaFuncSetAttribute(k_dc_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem + 1024);
+    // the owned rows' mat-vec reads are re-used from L1 column after column: smallest carveout
+    cudaFuncSetAttribute(k_dc_panel, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_dc_panel, DC_PT, psmem) != cudaSuccess || occ < 1)
         return -1;
-    const int G = sms;  // one CTA per SM (co-resident: cooperative launch)
+    const int G = std::min(sms, DC_MAXG);  // one CTA per SM (co-resident: cooperative launch)
+    if (n > DC_RPW * G * (DC_PT / 32)) return -1;  // rows per warp held in registers
     const int npan = (n + DC_NB - 2) / DC_NB;
+    const int nbt = std::max(1, (n - 1 + DC_BT - 1) / DC_BT);  // back-transform blocks
     size_t off = 0;
     auto take = [&](size_t cnt) {
         size_t o = off;
         off += (cnt + 3) & ~size_t(3);
         return o;
     };
-    const size_t oA = take(nl), oV = take(nl), oW = take((size_t)n * DC_NB), oy = take(n), owt = take(n),
+    const size_t oA = take(nl), oV = take(nl), oW = take(nl), oy = take(n), owt = take(n),
                  odv = take(n), oev = take(n), otau = take(n), opart = take((size_t)G * DC_PS), oQ0 = take(nl),
                  oQ1 = take(nl), oVT = take(nl), oD = take(n), opole = take(n), ozk = take(n), ozh = take(n),
-                 orho = take(mg.size() + 1), orot = take(2 * (size_t)n), oTm = take((size_t)std::max(npan, 1) * DC_NB * DC_NB),
-                 oX = take((size_t)DC_NB * ld), oY = take((size_t)DC_NB * ld), ocol = take(n), okc = take(mg.size() + 1),
+                 orho = take(mg.size() + 1), orot = take(2 * (size_t)n),
+                 oX = take((size_t)2 * DC_BT * ld), oY = take((size_t)DC_BT * ld),
+                 oG = take((size_t)nbt * DC_BT * DC_BT), oTb = take((size_t)nbt * DC_BT * DC_BT),
+                 ogd = take(nbt * ((sizeof(GemmArgs) + 7) / 8) + 2), ocol = take(n), okc = take(mg.size() + 1),
                  obnd = take(L + 1), operm = take(n), obar = take(1), omg = take(3 * mg.size() + 2),
                  odesc = take(mg.size() * ((sizeof(GemmArgs) + 7) / 8) + 2);
     double *base = nullptr;
@@ -815,7 +927,7 @@ static inline int dc_ws_alloc(DcWS &w, int n) {
     w.base = base;
     w.n = n;
     w.ld = ld;
-    w.G = G;
+    w.nctas = G;
     w.L = L;
     w.levels = levels;
     w.A = base + oA;
@@ -836,9 +948,12 @@ static inline int dc_ws_alloc(DcWS &w, int n) {
     w.zh = base + ozh;
     w.rhov = base + orho;
     w.rot = base + orot;
-    w.Tm = base + oTm;
     w.X = base + oX;
     w.Y = base + oY;
+    w.G = base + oG;
+    w.Tb = base + oTb;
+    w.gdesc = reinterpret_cast<GemmArgs *>(base + ((ogd + 1) & ~size_t(1)));
+    w.nbt = nbt;
     w.col = reinterpret_cast<int *>(base + ocol);
     w.kc = reinterpret_cast<int *>(base + okc);
     w.bnd = reinterpret_cast<int *>(base + obnd);
@@ -869,7 +984,27 @@ static inline int dc_ws_alloc(DcWS &w, int n) {
             desc[w.loff[l] + i] = a;
         }
     }
+    std::vector<GemmArgs> gd(nbt);
+    for (int b = 0; b < nbt; ++b) {  // G_b = V_b^T V_b over rows k0+1..n-1
+        const int k0 = b * DC_BT, nbb = std::max(0, std::min(DC_BT, n - 1 - k0)), r0 = k0 + 1;
+        GemmArgs a{};
+        a.M = a.N = nbb;
+        a.K = std::max(0, n - r0);
+        a.A = w.V + (size_t)r0 * ld + k0;
+        a.lda = ld;
+        a.TA = 1;
+        a.B = a.A;
+        a.ldb = ld;
+        a.TB = 0;
+        a.C = w.G + (size_t)b * DC_BT * DC_BT;
+        a.ldc = DC_BT;
+        a.alpha = 1.0;
+        a.beta = 0.0;
+        a.a16 = a.b16 = (reinterpret_cast<uintptr_t>(a.A) & 15) == 0;
+        gd[b] = a;
+    }
     bool ok = cudaMemset(base, 0, off * sizeof(double)) == cudaSuccess;
+    ok = ok && cudaMemcpy(w.gdesc, gd.data(), sizeof(GemmArgs) * nbt, cudaMemcpyHostToDevice) == cudaSuccess;
     ok = ok && cudaMemcpy(w.bnd, bnd.data(), sizeof(int) * (L + 1), cudaMemcpyHostToDevice) == cudaSuccess;
     if (!mg.empty()) {
         ok = ok && cudaMemcpy(w.mg, mg.data(), sizeof(DcMerge) * mg.size(), cudaMemcpyHostToDevice) == cudaSuccess;
@@ -878,6 +1013,8 @@ static inline int dc_ws_alloc(DcWS &w, int n) {
     const size_t dsm = (size_t)DC_NMAX * 12 + (size_t)DC_NMAX * 16 + (size_t)DC_NMAX * 16 + 64;
     ok = ok && cudaFuncSetAttribute(k_dc_deflate, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm) == cudaSuccess;
     ok = ok && cudaFuncSetAttribute(k_dc_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, DC_NMAX * 12) == cudaSuccess;
+    ok = ok && cudaFuncSetAttribute(k_dc_tblock, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)(sizeof(double) * DC_BT * (DC_BT + 1))) == cudaSuccess;
     if (!ok) {
         dc_ws_free(w);
         return -1;
@@ -961,14 +1098,33 @@ static inline int dc_eigh(DcWS &w, const double *H, int ldh, int n, double *lam,
         a.bar = w.bar;
         cudaMemsetAsync(w.bar, 0, sizeof(unsigned), s);
         void *args[] = {&a};
-        if (cudaLaunchCooperativeKernel((void *)k_dc_panel, w.G, DC_PT, args, sizeof(double) * n, s) != cudaSuccess)
+        if (cudaLaunchCooperativeKernel((void *)k_dc_panel, w.nctas, DC_PT, args, sizeof(double) * n, s) != cudaSuccess)
             return -1;
         const int r0 = k0 + nbp, m = n - r0;
-        if (m > 0) {  // A22 -= V W^T + W V^T
+        if (m > 0) {  // A22 -= V W^T + W V^T: one K = 2 nbp GEMM, [V W] [W V]^T by the K-split gather
             double *A22 = w.A + (size_t)r0 * ld + r0;
-            const double *Vp = w.V + (size_t)r0 * ld + k0, *Wp = w.W + (size_t)r0 * DC_NB;
-            dc_gemm(m, m, nbp, Vp, ld, 0, Wp, DC_NB, 1, A22, ld, -1.0, 1.0, s);
-            dc_gemm(m, m, nbp, Wp, DC_NB, 0, Vp, ld, 1, A22, ld, -1.0, 1.0, s);
+            const double *Vp = w.V + (size_t)r0 * ld + k0, *Wp = w.W + (size_t)r0 * ld;
+            if (nbp % GM_BK == 0) {
+                GemmArgs g{};
+                g.M = g.N = m;
+                g.K = 2 * nbp;
+                g.A = Vp;
+                g.A2 = Wp;
+                g.lda = ld;
+                g.B = Wp;
+                g.B2 = Vp;
+                g.ldb = ld;
+                g.TB = 1;
+                g.ksplit = nbp;
+                g.C = A22;
+                g.ldc = ld;
+                g.alpha = -1.0;
+                g.beta = 1.0;
+                gemm_launch(g, s);
+            } else {
+                dc_gemm(m, m, nbp, Vp, ld, 0, Wp, ld, 1, A22, ld, -1.0, 1.0, s);
+                dc_gemm(m, m, nbp, Wp, ld, 0, Vp, ld, 1, A22, ld, -1.0, 1.0, s);
+            }
         }
     }
     k_dc_last_diag<<<1, 32, 0, s>>>(w.A, ld, n, w.dv);
@@ -1002,15 +1158,41 @@ static inline int dc_eigh(DcWS &w, const double *H, int ldh, int n, double *lam,
     if (prof) cudaEventRecord(ev[2], s);
     dc_dump("D", w.D, n, s);
     dc_dump("Z", Z, nl, s);
-    // ---- stage 3: Z <- Q_H Z, panels last to first
-    const int npan = (n + DC_NB - 2) / DC_NB;
-    k_dc_tmat<<<npan, 1024, 0, s>>>(w.V, ld, n, w.tau, w.Tm);
-    for (int p = npan - 1; p >= 0; --p) {
-        const int k0 = p * DC_NB, nbp = std::min(DC_NB, n - 1 - k0), r0 = k0 + 1, m = n - r0;
-        const double *Vp = w.V + (size_t)r0 * ld + k0;
-        dc_gemm(nbp, n, m, Vp, ld, 1, Z + (size_t)r0 * ld, ld, 0, w.X, ld, 1.0, 0.0, s);        // X = V^T Z
-        dc_gemm(nbp, n, nbp, w.Tm + (size_t)p * DC_NB * DC_NB, DC_NB, 0, w.X, ld, 0, w.Y, ld, 1.0, 0.0, s);  // Y = T X
-        dc_gemm(m, n, nbp, Vp, ld, 0, w.Y, ld, 0, Z + (size_t)r0 * ld, ld, -1.0, 1.0, s);      // Z -= V Y
+    // ---- stage 3: Z <- Q_H Z, blocks of DC_BT reflectors last to first
+    if (gemm_launch_batched<1, 0>(w.gdesc, w.nbt, DC_BT, DC_BT, s) != cudaSuccess) return -1;
+    k_dc_tblock<<<w.nbt, DC_BT, sizeof(double) * DC_BT * (DC_BT + 1), s>>>(w.G, w.tau, n, w.Tb);
+    for (int b = w.nbt - 1; b >= 0; --b) {
+        const int k0 = b * DC_BT, nbb = std::min(DC_BT, n - 1 - k0), r0 = k0 + 1, m = n - r0;
+        if (nbb <= 0) continue;
+        const double *Vb = w.V + (size_t)r0 * ld + k0, *Tb = w.Tb + (size_t)b * DC_BT * DC_BT;
+        double *X0 = w.X, *X1 = w.X + (size_t)DC_BT * ld;
+        const int mh = (m / 2) & ~31;
+        if (nbb % GM_BK == 0 && mh >= 64) {
+            // split-K: X0 = V_b^T Z over the first mh rows, X1 over the rest; Y = [T T][X0; X1]
+            dc_gemm(nbb, n, mh, Vb, ld, 1, Z + (size_t)r0 * ld, ld, 0, X0, ld, 1.0, 0.0, s);
+            dc_gemm(nbb, n, m - mh, Vb + (size_t)mh * ld, ld, 1, Z + (size_t)(r0 + mh) * ld, ld, 0, X1, ld, 1.0, 0.0,
+                    s);
+            GemmArgs g{};
+            g.M = nbb;
+            g.N = n;
+            g.K = 2 * nbb;
+            g.A = Tb;
+            g.A2 = Tb;
+            g.lda = DC_BT;
+            g.B = X0;
+            g.B2 = X1;
+            g.ldb = ld;
+            g.ksplit = nbb;
+            g.C = w.Y;
+            g.ldc = ld;
+            g.alpha = 1.0;
+            g.beta = 0.0;
+            gemm_launch(g, s);
+        } else {
+            dc_gemm(nbb, n, m, Vb, ld, 1, Z + (size_t)r0 * ld, ld, 0, X0, ld, 1.0, 0.0, s);   // X = V^T Z
+            dc_gemm(nbb, n, nbb, Tb, DC_BT, 0, X0, ld, 0, w.Y, ld, 1.0, 0.0, s);             // Y = T X
+        }
+        dc_gemm(m, n, nbb, Vb, ld, 0, w.Y, ld, 0, Z + (size_t)r0 * ld, ld, -1.0, 1.0, s);   // Z -= V Y
     }
     k_dc_sort<<<1, 1024, (size_t)12 * DC_NMAX, s>>>(w.D, n, lam, w.perm);
     k_dc_gather<<<148 * 4, 256, 0, s>>>(Z, ld, w.perm, n, psi, ldp);
