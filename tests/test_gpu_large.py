@@ -154,3 +154,42 @@ def test_block_jacobi_cold_decomposition(large_case):
     assert np.max(np.abs(np.sort(lam) - ref)) < 1e-11 * fro
     assert np.max(np.abs(psi.T @ psi - np.eye(d))) < 1e-11
     assert np.linalg.norm(psi @ np.diag(lam) @ psi.T - hs) < 1e-11 * fro
+
+
+def test_dc_cold_decomposition(large_case):
+    """cold_order="dc": the chain-start decomposition by Householder tridiagonalisation + divide
+    and conquer (sgp_dc.cuh) against LAPACK, as the block-Jacobi test above; eigenvalues come
+    out ascending."""
+    from paper_2511_06407_b200 import _native as nat
+
+    model, data, target, _ = large_case
+    d = target.dim
+    q = np.zeros((1, d))
+    h = target.device.eval(1.0, q, nat.EVAL_HESSIAN)["hess"][0]
+    hs = 0.5 * (h + h.T)
+    cfg = S.ChainConfig(epsilon=0.002, leapfrogs=1, moves=1, burnin=0, warm_order="refine", cold_order="dc")
+    ch = S.DeviceChains(target.device, np.ones(1), cfg)
+    ch.set_q(q)
+    ch.init()
+    assert ch.status_host()[0] == 0
+    lam = ch.lam.cpu().numpy()[0]
+    psi = ch.psi.cpu().numpy()[0]
+    ref = np.linalg.eigvalsh(hs)
+    fro = np.linalg.norm(hs)
+    assert np.all(np.diff(lam) >= 0.0)
+    assert np.max(np.abs(lam - ref)) < 1e-12 * fro
+    assert np.max(np.abs(psi.T @ psi - np.eye(d))) < 1e-12
+    assert np.linalg.norm(psi @ np.diag(lam) @ psi.T - hs) < 1e-12 * fro
+
+
+def test_large_chain_with_dc_cold_starts_like_oracle(large_case):
+    """A chain whose cold decompositions (start, rejections) use the divide and conquer: the
+    starting Hamiltonian is Psi-invariant, so it equals the reference algorithm's."""
+    model, data, target, ot = large_case
+    cfg = S.ChainConfig(epsilon=0.002, leapfrogs=2, moves=3, burnin=0, seed=5, record_q=True,
+                        warm_order="refine", cold_order="dc")
+    res = S.run_chain(target, cfg)
+    ref = oracle.run_chain(ot, oracle.OConfig(epsilon=0.002, leapfrogs=2, moves=1, burnin=0, seed=5))
+    assert res.records[0].h_before == pytest.approx(ref.records[0].h_before, rel=1e-10)
+    assert all(np.isfinite(r.h_after) for r in res.records)
+    assert res.accept_count >= 2

@@ -64,8 +64,9 @@ def _gpu_mean_se(draws):
     return cm.mean(axis=0), cm.std(axis=0, ddof=1) / np.sqrt(cm.shape[0])
 
 
-def _gpu_draws(target, order, n_chains, moves, seed0=7000):
-    cfg = S.ChainConfig(epsilon=EPS, leapfrogs=LF, moves=moves, burnin=0, record_q=True, warm_order=order)
+def _gpu_draws(target, order, n_chains, moves, seed0=7000, cold="cyclic"):
+    cfg = S.ChainConfig(epsilon=EPS, leapfrogs=LF, moves=moves, burnin=0, record_q=True, warm_order=order,
+                        cold_order=cold)
     res = S.run_chains(target, cfg, [seed0 + z for z in range(n_chains)])
     ok = [r for r in res if not isinstance(r, Exception)]  # a chain may diverge on its first move
     assert len(ok) >= 0.9 * n_chains
@@ -86,12 +87,14 @@ def test_posterior_moments_match_reference(problem, reference_draws, order):
     _assert_same_distribution(gpu, reference_draws)
 
 
-def test_refine_solver_posterior_moments_match_reference(problem, reference_draws, monkeypatch):
+@pytest.mark.parametrize("cold", ["cyclic", "dc"])
+def test_refine_solver_posterior_moments_match_reference(problem, reference_draws, monkeypatch, cold):
     """The large-d path (host-sequenced leapfrog, DMMA GEMMs, eigenvector refinement) forced
-    onto the d = 14 model."""
+    onto the d = 14 model; cold decompositions (start, rejections) in the reference order or by
+    tridiagonalisation + divide and conquer."""
     monkeypatch.setenv("SGP_FORCE_LARGE", "1")
     model, data = problem
-    gpu = _gpu_draws(PosteriorTarget(model, data), "refine", n_chains=6, moves=400)
+    gpu = _gpu_draws(PosteriorTarget(model, data), "refine", n_chains=6, moves=400, cold=cold)
     _assert_same_distribution(gpu, reference_draws)
 
 
