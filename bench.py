@@ -453,7 +453,7 @@ def run_gpu_c4(args):
     d = target.dim
     C = args.leapfrogs or C4_LEAPFROGS
     cfg = ChainConfig(epsilon=C4_EPS, leapfrogs=C, moves=1, burnin=0, warm_order=args.warm_order or "refine",
-                      cold_order="cyclic")
+                      cold_order=getattr(args, "cold_order", "cyclic"))
     Z = 1
     chains = DeviceChains(target.device, np.ones(Z), cfg)
     chains.set_q(np.zeros((Z, d)))
@@ -936,6 +936,9 @@ def main():
     ap.add_argument("--chains-per-sm", type=int, default=12)
     ap.add_argument("--warm-order", default=None, choices=["cyclic", "parallel", "refine"],
                     help="warm eigensolver (C4 default refine, C2 default cyclic)")
+    ap.add_argument("--cold-order", default="cyclic", choices=["cyclic", "parallel", "dc"],
+                    help="C4 cold decompositions (chain start, rejections): reference order (default) or "
+                         "tridiagonalisation + divide and conquer")
     ap.add_argument("--ref-leapfrogs", type=int, default=20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ess-moves", type=int, default=300, help="recorded moves of the min-ESS pilot (0: skip)")
