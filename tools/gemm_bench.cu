@@ -1,5 +1,8 @@
 // Correctness and throughput of the DMMA GEMM (sgp_gemm.cuh).
-// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -o tools/gemm_bench tools/gemm_bench.cu
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -o tools/gemm_bench tools/gemm_bench.cu -lcublas
+// Throughput cases use random operands (zero operands draw less power and run at higher clocks)
+// and time cuBLAS DGEMM on the same shapes (row-major C = A B as column-major C^T = B^T A^T).
+#include <cublas_v2.h>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -21,8 +24,20 @@ static void ref(const GemmArgs &g, const std::vector<double> &A, const std::vect
         }
 }
 
+__global__ void k_fill(double *p, size_t n, unsigned seed) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+        unsigned x = (unsigned)i * 2654435761u ^ seed;
+        x ^= x >> 13;
+        x *= 0x5bd1e995u;
+        x ^= x >> 15;
+        p[i] = (x & 0xffffff) / 16777216.0 - 0.5;
+    }
+}
+
 int main() {
     int fails = 0;
+    cublasHandle_t hb;
+    cublasCreate(&hb);
     for (int ta = 0; ta < 2; ++ta)
         for (int tb = 0; tb < 2; ++tb)
             for (int sc = 0; sc < 2; ++sc) {
@@ -118,16 +133,30 @@ int main() {
         double *dA, *dB, *dC, *dS = nullptr;
         size_t na = (size_t)(c.ta ? c.K : c.M) * g.lda, nb = (size_t)(c.tb ? c.N : c.K) * g.ldb;
         cudaMalloc(&dA, na * 8); cudaMalloc(&dB, nb * 8); cudaMalloc(&dC, (size_t)c.M * g.ldc * 8);
-        cudaMemset(dA, 0, na * 8); cudaMemset(dB, 0, nb * 8);
-        if (c.sc) { cudaMalloc(&dS, c.K * 8); cudaMemset(dS, 0, c.K * 8); }
+        k_fill<<<592, 256>>>(dA, na, 1u); k_fill<<<592, 256>>>(dB, nb, 2u);
+        if (c.sc) { cudaMalloc(&dS, c.K * 8); k_fill<<<16, 256>>>(dS, c.K, 3u); }
         g.A = dA; g.B = dB; g.C = dC; g.scale = dS;
+        g.a16 = (g.lda % 2 == 0); g.b16 = (g.ldb % 2 == 0);
         gemm_launch(g, 0);
         cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
         cudaEventRecord(e0);
         for (int r = 0; r < 5; ++r) gemm_launch(g, 0);
         cudaEventRecord(e1); cudaEventSynchronize(e1);
         float ms; cudaEventElapsedTime(&ms, e0, e1); ms /= 5;
-        printf("%-40s %8.3f ms  %6.2f TFLOP/s\n", c.name, ms, 2.0 * c.M * c.N * (double)c.K / (ms * 1e-3) / 1e12);
+        // cuBLAS: C^T (N x M, ld ldc) = op(B)^T op(A)^T in column-major terms
+        const double one = 1.0, zero = 0.0;
+        auto cub = [&]() {
+            cublasDgemm(hb, c.tb ? CUBLAS_OP_T : CUBLAS_OP_N, c.ta ? CUBLAS_OP_T : CUBLAS_OP_N, c.N, c.M, c.K, &one, dB,
+                        g.ldb, dA, g.lda, &zero, dC, g.ldc);
+        };
+        cub();
+        cudaEventRecord(e0);
+        for (int r = 0; r < 5; ++r) cub();
+        cudaEventRecord(e1); cudaEventSynchronize(e1);
+        float mc; cudaEventElapsedTime(&mc, e0, e1); mc /= 5;
+        const double fl = 2.0 * c.M * c.N * (double)c.K;
+        printf("%-40s ours %8.3f ms %6.2f TF/s | cuBLAS %8.3f ms %6.2f TF/s\n", c.name, ms, fl / (ms * 1e-3) / 1e12, mc,
+               fl / (mc * 1e-3) / 1e12);
         cudaFree(dA); cudaFree(dB); cudaFree(dC); if (dS) cudaFree(dS);
     }
     printf(fails ? "FAIL\n" : "OK\n");
