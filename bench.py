@@ -898,14 +898,14 @@ def run_gpu(args):
             line["roofline"]["peaks_file"] = "MEASURED_PEAKS.json present (bf16/HBM only)"
         # DRAM bytes per launch of this kernel from the committed ncu --set full capture
         # of the same command (profiles/), when it was taken on this configuration
-        tpath = os.path.join(ROOT, "profiles", "r1_traffic_k_run_moves.json")
+        tpath = os.path.join(ROOT, "profiles", "r2_traffic_k_run_moves.json")
         if os.path.exists(tpath):
             with open(tpath) as f:
                 tr = json.load(f)
             if tr.get("chains") == Z and tr.get("leapfrogs") == LEAPFROGS:
                 line["roofline"]["traffic"] = tr["dram_bytes_per_launch"]
                 line["roofline"]["traffic_unit"] = "bytes/launch (DRAM read+write, ncu)"
-                line["roofline"]["traffic_source"] = "profiles/r1_traffic_k_run_moves.json"
+                line["roofline"]["traffic_source"] = "profiles/r2_traffic_k_run_moves.json"
         if world == 1 and not args.no_cpu_baseline:
             cores = os.cpu_count() or 1
             pool = CpuPool(cores)

@@ -335,7 +335,10 @@ static ChainLaunch chain_launch(const sgp_model *m) {
     }
     ChainLaunch L;
     L.nt = nt;
-    L.per_sm = nt == 32 ? 12 : (nt == 64 ? 6 : (nt == 128 ? 4 : 2));
+    // 64-thread CTAs: four per SM.  Six fit the registers, but at four the larger shared-memory
+    // budget keeps more of each chain's matrices on chip: same C2 throughput, DRAM traffic
+    // 42 -> 9.8 GB per bench launch (profiles/r2_traffic_k_run_moves.json)
+    L.per_sm = nt == 32 ? 12 : (nt == 64 ? 4 : (nt == 128 ? 4 : 2));
     const char *eps = getenv("SGP_CHAINS_PER_SM");
     if (eps && atoi(eps) > 0) L.per_sm = atoi(eps);
     const char *ech = getenv("SGP_STAGE_CH");
