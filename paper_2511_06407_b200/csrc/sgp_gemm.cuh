@@ -286,13 +286,27 @@ __global__ void __launch_bounds__(GM_THREADS_MAX) k_gemm_dmma_batched(const Gemm
     gm_body<TA, TB, GmSmall>(g);
 }
 
-// mirror the upper triangle of an n x n matrix into the lower one
-__global__ void k_mirror_upper(double *C, int n, int ldc) {
-    for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < (size_t)n * n;
-         idx += (size_t)gridDim.x * blockDim.x) {
-        const int i = (int)(idx / n), j = (int)(idx - (size_t)i * n);
-        if (i > j) C[(size_t)i * ldc + j] = C[(size_t)j * ldc + i];
+// mirror the upper triangle of an n x n matrix into the lower one: tile (ti, tj), ti >= tj, of
+// the lower triangle is the transpose of upper tile (tj, ti), staged through shared memory so
+// both the read and the write are coalesced.  Launch: grid (nt, nt), block (32, 8).
+__global__ void k_mirror_upper_tiled(double *C, int n, int ldc) {
+    __shared__ double t[32][33];
+    const int ti = blockIdx.y, tj = blockIdx.x;
+    if (ti < tj) return;
+    const int r0 = tj * 32, c0 = ti * 32;  // source tile (upper): rows r0.., columns c0..
+    for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+        const int r = r0 + k, c = c0 + threadIdx.x;
+        if (r < n && c < n) t[k][threadIdx.x] = C[(size_t)r * ldc + c];
     }
+    __syncthreads();
+    for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+        const int r = c0 + k, c = r0 + threadIdx.x;  // destination (lower): row r > column c
+        if (r < n && c < n && r > c) C[(size_t)r * ldc + c] = t[threadIdx.x][k];
+    }
+}
+static inline void mirror_upper(double *C, int n, int ldc, cudaStream_t s) {
+    const int nt = (n + 31) / 32;
+    k_mirror_upper_tiled<<<dim3(nt, nt), dim3(32, 8), 0, s>>>(C, n, ldc);
 }
 
 template <int TA, int TB, class CFG>

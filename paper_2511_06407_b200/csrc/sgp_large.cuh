@@ -32,7 +32,8 @@ struct LgPtrs {
     double *bjU, *bjLam, *bjPart;
     int *bjCnt;
     GemmArgs *bjDesc;            // [round][col A | row A | col V even | col V odd][2 * pairs]
-    GemmArgs *hdesc;             // the likelihood-Hessian blocks' batched GEMM descriptors (3)
+    GemmArgs *hdesc;             // the likelihood-Hessian blocks' batched GEMM descriptors (4)
+    double *hpart;               // second K half of the off-diagonal likelihood block (J = 2)
     // host handles owned by this workspace (one per model, like the buffers above): the
     // high-priority stream of the block-Jacobi A chain and the events ordering it against
     // the caller's stream (in, solved, chain, V update of even / odd rounds)
@@ -42,6 +43,8 @@ struct LgPtrs {
     JbWS *jb;
     // tridiagonalisation + divide and conquer workspace (cold_order="dc"), allocated on first use
     DcWS *dc;
+    // pinned host staging of the scalars read back at every host decision (lg_sync)
+    double *hsync;
 };
 
 static void lg_free_handles(LgPtrs &L) {
@@ -55,6 +58,8 @@ static void lg_free_handles(LgPtrs &L) {
         delete L.dc;
         L.dc = nullptr;
     }
+    if (L.hsync) cudaFreeHost(L.hsync);
+    L.hsync = nullptr;
     if (L.bj_hs) cudaStreamDestroy(L.bj_hs);
     for (cudaEvent_t &e : L.bj_ev)
         if (e) cudaEventDestroy(e);
@@ -116,6 +121,8 @@ struct LgOpArgs {
     double tau;
 };
 
+// one instantiation per op (OP only names the kernel, so profiles attribute time per op)
+template <int OP>
 __global__ void __launch_bounds__(LG_NT) k_lg_op(LgPtrs L, LgOpArgs a) {
     __shared__ __align__(16) char smem[128 * sizeof(double)];
     ChainWS w;
@@ -215,7 +222,8 @@ __global__ void k_lg_mmat(LgPtrs L, int slot, double kappa, double c1, int with_
     const double *b = L.vec + (size_t)10 * d;
     for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < (size_t)d * d;
          idx += (size_t)gridDim.x * blockDim.x) {
-        const int j = (int)(idx / d), l = (int)(idx - (size_t)j * d);
+        const unsigned u_ = (unsigned)idx;  // idx < d^2 < 2^32: 32-bit division
+        const int j = (int)(u_ / (unsigned)d), l = (int)(u_ - (unsigned)j * (unsigned)d);
         double m = 0.0;
         if (with_w1) {
             const double diff = lam[j] - lam[l];
@@ -230,7 +238,8 @@ __global__ void k_lg_mmat(LgPtrs L, int slot, double kappa, double c1, int with_
 __global__ void k_lg_symmetrize(double *A, int d) {
     for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < (size_t)d * d;
          idx += (size_t)gridDim.x * blockDim.x) {
-        const int i = (int)(idx / d), j = (int)(idx - (size_t)i * d);
+        const unsigned u_ = (unsigned)idx;  // idx < d^2 < 2^32: 32-bit division
+        const int i = (int)(u_ / (unsigned)d), j = (int)(u_ - (unsigned)i * (unsigned)d);
         if (i < j) {
             const double v = 0.5 * (A[idx] + A[(size_t)j * d + i]);
             A[idx] = v;
@@ -380,8 +389,31 @@ __global__ void k_lg_transpose_block(double *H, int d, int r0, int c0, int nr, i
     // H[c0 + j][r0 + i] = H[r0 + i][c0 + j]
     for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < (size_t)nr * nc;
          idx += (size_t)gridDim.x * blockDim.x) {
-        const int i = (int)(idx / nc), j = (int)(idx - (size_t)i * nc);
+        const unsigned u_ = (unsigned)idx;  // idx < nc^2 < 2^32: 32-bit division
+        const int i = (int)(u_ / (unsigned)nc), j = (int)(u_ - (unsigned)i * (unsigned)nc);
         H[(size_t)(c0 + j) * d + r0 + i] = H[(size_t)(r0 + i) * d + c0 + j];
+    }
+}
+
+// off-diagonal likelihood block computed as two K halves: H[r0+i][c0+j] += P[i][j] (P: the
+// second half, nr x nc, leading dimension ldp), then mirrored into H[c0+j][r0+i]; 32 x 32 tiles
+// through shared memory so both the row and the mirrored column side are coalesced
+__global__ void k_lg_addt_block(double *H, int d, int r0, int c0, int nr, int nc, const double *P, int ldp) {
+    __shared__ double t[32][33];
+    const int ti = blockIdx.y * 32, tj = blockIdx.x * 32;
+    for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+        const int i = ti + k, j = tj + threadIdx.x;
+        if (i < nr && j < nc) {
+            double *h = H + (size_t)(r0 + i) * d + c0 + j;
+            const double v = *h + P[(size_t)i * ldp + j];
+            *h = v;
+            t[k][threadIdx.x] = v;
+        }
+    }
+    __syncthreads();
+    for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+        const int j = tj + k, i = ti + threadIdx.x;
+        if (i < nr && j < nc) H[(size_t)(c0 + j) * d + r0 + i] = t[threadIdx.x][k];
     }
 }
 
@@ -451,7 +483,8 @@ __global__ void k_lg_mgs_step(double *X, int d, int i, double *nrm) {
 __global__ void k_lg_mirror_block(double *H, int d, int o, int n) {
     for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < (size_t)n * n;
          idx += (size_t)gridDim.x * blockDim.x) {
-        const int i = (int)(idx / n), j = (int)(idx - (size_t)i * n);
+        const unsigned u_ = (unsigned)idx;  // idx < n^2 < 2^32: 32-bit division
+        const int i = (int)(u_ / (unsigned)n), j = (int)(u_ - (unsigned)i * (unsigned)n);
         if (i > j) H[(size_t)(o + i) * d + o + j] = H[(size_t)(o + j) * d + o + i];
     }
 }
@@ -478,22 +511,47 @@ __global__ void k_lg_set2(double *dst, double a, double b) {
 // ---- grid-wide O(N d) glue ------------------------------------------------
 // latent values and per-sample derivatives; block partial sums of U and a
 // non-finite flag into red[blockIdx.x], red[gridDim.x + blockIdx.x]
+// f = Phi q and the per-sample likelihood fields.  32 samples per CTA (one per lane, coalesced
+// feature-major Phi rows); the 8 warps split the features with four accumulators each, so
+// 8192 samples keep 2048 warps streaming Phi (136 MB at C4) instead of 256 serial dot products.
+#define LG_LIK_SPB 32
 __global__ void __launch_bounds__(256) k_lg_lik(LgPtrs L, const double *q) {
+    __shared__ double part[2][8][LG_LIK_SPB + 1];
     __shared__ double red[64];
     const ModelParams &mp = L.M.mp;
-    const int ld = mp.ld;
+    const int ld = mp.ld, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int i = blockIdx.x * LG_LIK_SPB + lane;
+    for (int j = 0; j < mp.J; ++j) {
+        const int D = mp.D[j], a0 = (D * warp) / 8, a1 = (D * (warp + 1)) / 8;
+        const double *ph = L.M.phi + (size_t)(j ? mp.D[0] : 0) * ld + i;
+        const double *qq = q + (j ? mp.fstart[1] : 0);
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+        if (i < ld) {
+            int a = a0;
+            for (; a + 3 < a1; a += 4) {
+                s0 = fma(ph[(size_t)a * ld], qq[a], s0);
+                s1 = fma(ph[(size_t)(a + 1) * ld], qq[a + 1], s1);
+                s2 = fma(ph[(size_t)(a + 2) * ld], qq[a + 2], s2);
+                s3 = fma(ph[(size_t)(a + 3) * ld], qq[a + 3], s3);
+            }
+            for (; a < a1; ++a) s0 = fma(ph[(size_t)a * ld], qq[a], s0);
+        }
+        part[j][warp][lane] = (s0 + s1) + (s2 + s3);
+    }
+    __syncthreads();
     double su = 0.0, bad = 0.0;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < ld; i += gridDim.x * blockDim.x) {
+    if (warp == 0 && i < ld) {
         double f0 = 0.0, f1 = 0.0;
-        for (int a = 0; a < mp.D[0]; ++a) f0 += L.M.phi[(size_t)a * ld + i] * q[a];
-        if (mp.J == 2)
-            for (int a = 0; a < mp.D[1]; ++a) f1 += L.M.phi[(size_t)(mp.D[0] + a) * ld + i] * q[mp.fstart[1] + a];
+        for (int w = 0; w < 8; ++w) {
+            f0 += part[0][w][lane];
+            if (mp.J == 2) f1 += part[1][w][lane];
+        }
         if (i < mp.N) {
             if (!isfinite(f0) || !isfinite(f1)) bad = 1.0;
             L.S[F_F0 * ld + i] = f0;
             L.S[F_F1 * ld + i] = f1;
             lik_sample(mp.lik, mp.vfloor, L.M.y[i], f0, f1, L.S, ld, i);
-            su += L.S[F_U * ld + i];
+            su = L.S[F_U * ld + i];
         } else {
             for (int k = 0; k < F_COUNT; ++k) L.S[k * ld + i] = 0.0;
         }
@@ -529,9 +587,16 @@ __global__ void k_lg_project(LgPtrs L, double tau, int field0, int field1, doubl
         const int f = (a < mp.D[0]) ? field0 : field1;
         const double *pr = L.M.phi + (size_t)a * ld;
         const double *sr = L.S + (size_t)f * ld;
-        double s = 0.0;
-        for (int i = lane; i < mp.N; i += 32) s += pr[i] * sr[i];
-        s = warp_sum(s);
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+        int i = lane;
+        for (; i + 96 < mp.N; i += 128) {
+            s0 += pr[i] * sr[i];
+            s1 += pr[i + 32] * sr[i + 32];
+            s2 += pr[i + 64] * sr[i + 64];
+            s3 += pr[i + 96] * sr[i + 96];
+        }
+        for (; i < mp.N; i += 32) s0 += pr[i] * sr[i];
+        const double s = warp_sum((s0 + s1) + (s2 + s3));
         if (lane == 0) out[a] = tau * s;
     }
 }
@@ -755,15 +820,23 @@ __global__ void k_bj_offnorm(const double *A, int dp, double *part) {
     }
 }
 // ---- grid mat-vecs of the metric algebra (metric.py:188-241) at large d ----
-#define LG_TV_KS 16
+#define LG_TV_KS 32
 // part[ks][j] = sum_{k in chunk ks} P[k][j] v[k]   (Psi^T v, coalesced over j)
 __global__ void k_lg_tvec_part(const double *P, const double *v, int d, double *part) {
     const int j = blockIdx.x * blockDim.x + threadIdx.x, ks = blockIdx.y;
     const int chunk = (d + LG_TV_KS - 1) / LG_TV_KS, k0 = ks * chunk, k1 = min(d, k0 + chunk);
     if (j >= d) return;
-    double s = 0.0;
-    for (int k = k0; k < k1; ++k) s += P[(size_t)k * d + j] * v[k];
-    part[(size_t)ks * d + j] = s;
+    // four independent accumulators: the loads of four rows are in flight together
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    int k = k0;
+    for (; k + 3 < k1; k += 4) {
+        s0 += P[(size_t)k * d + j] * v[k];
+        s1 += P[(size_t)(k + 1) * d + j] * v[k + 1];
+        s2 += P[(size_t)(k + 2) * d + j] * v[k + 2];
+        s3 += P[(size_t)(k + 3) * d + j] * v[k + 3];
+    }
+    for (; k < k1; ++k) s0 += P[(size_t)k * d + j] * v[k];
+    part[(size_t)ks * d + j] = (s0 + s1) + (s2 + s3);
 }
 // out[j] = f(sum_ks part[ks][j]): mode 0: /g, 1: *g, 3: plain; 4: kinetic terms t^2/g into out
 __global__ void k_lg_tvec_fin(const double *part, const double *g, int d, int mode, double *out) {
@@ -777,9 +850,17 @@ __global__ void k_lg_tvec_fin(const double *part, const double *g, int d, int mo
 __global__ void k_lg_vec(const double *P, const double *t, int d, double *out) {
     const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, l = threadIdx.x & 31;
     if (w >= d) return;
-    double s = 0.0;
-    for (int k = l; k < d; k += 32) s += P[(size_t)w * d + k] * t[k];
-    s = warp_sum(s);
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    const double *row = P + (size_t)w * d;
+    int k = l;
+    for (; k + 96 < d; k += 128) {
+        s0 += row[k] * t[k];
+        s1 += row[k + 32] * t[k + 32];
+        s2 += row[k + 64] * t[k + 64];
+        s3 += row[k + 96] * t[k + 96];
+    }
+    for (; k < d; k += 32) s0 += row[k] * t[k];
+    const double s = warp_sum((s0 + s1) + (s2 + s3));
     if (l == 0) out[w] = s;
 }
 __global__ void k_lg_sqrtg_v(const double *g, const double *v, int d, double *out) {
@@ -836,7 +917,8 @@ __global__ void k_bj_offnorm_final(const double *part, int n, double *out) {
 __global__ void k_bj_in(double *Ap, double *Vp, const double *H, const double *P, int d, int dp, int identity) {
     for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < (size_t)dp * dp;
          idx += (size_t)gridDim.x * blockDim.x) {
-        const int i = (int)(idx / dp), j = (int)(idx - (size_t)i * dp);
+        const unsigned u_ = (unsigned)idx;  // idx < dp^2 < 2^32: 32-bit division
+        const int i = (int)(u_ / (unsigned)dp), j = (int)(u_ - (unsigned)i * (unsigned)dp);
         const bool in = i < d && j < d;
         Ap[idx] = in ? H[(size_t)i * d + j] : 0.0;
         Vp[idx] = in ? (identity ? (i == j ? 1.0 : 0.0) : P[(size_t)i * d + j]) : (i == j ? 1.0 : 0.0);
@@ -845,7 +927,8 @@ __global__ void k_bj_in(double *Ap, double *Vp, const double *H, const double *P
 __global__ void k_bj_out(double *H, double *P, const double *Ap, const double *Vp, int d, int dp) {
     for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < (size_t)d * d;
          idx += (size_t)gridDim.x * blockDim.x) {
-        const int i = (int)(idx / d), j = (int)(idx - (size_t)i * d);
+        const unsigned u_ = (unsigned)idx;  // idx < d^2 < 2^32: 32-bit division
+        const int i = (int)(u_ / (unsigned)d), j = (int)(u_ - (unsigned)i * (unsigned)d);
         P[idx] = Vp[(size_t)i * dp + j];
         if (i == j) H[idx] = Ap[(size_t)i * dp + j];
     }
@@ -936,10 +1019,37 @@ static void lg_op(LgCtx &c, int op, int slot = 0, int a0 = 0, int a1 = 0, int i0
     a.eps = eps;
     a.cfg = c.cfg;
     a.tau = c.tau;
-    k_lg_op<<<1, LG_NT, 0, c.s>>>(c.L, a);
+    switch (op) {
+#define LG_OP_CASE(K) \
+    case K:           \
+        k_lg_op<K><<<1, LG_NT, 0, c.s>>>(c.L, a); \
+        break;
+        LG_OP_CASE(LG_STATE)
+        LG_OP_CASE(LG_TRACE)
+        LG_OP_CASE(LG_GLAM)
+        LG_OP_CASE(LG_COLD)
+        LG_OP_CASE(LG_OFFNORM)
+        LG_OP_CASE(LG_LOADFRAME)
+        LG_OP_CASE(LG_QDELTA)
+        LG_OP_CASE(LG_PHALF)
+        LG_OP_CASE(LG_JCYC)
+#undef LG_OP_CASE
+        default:
+            k_lg_op<-1><<<1, LG_NT, 0, c.s>>>(c.L, a);
+    }
 }
 
 static int lg_sync(LgCtx &c) {
+    if (c.L.hsync) {
+        // sc, si and status are adjacent in the workspace: one copy into pinned staging
+        const size_t n = (size_t)(reinterpret_cast<const double *>(c.L.status) - c.L.sc) + 1;
+        cudaMemcpyAsync(c.L.hsync, c.L.sc, sizeof(double) * n, cudaMemcpyDeviceToHost, c.s);
+        if (cudaStreamSynchronize(c.s) != cudaSuccess) return -1;
+        memcpy(c.sc, c.L.hsync, sizeof(c.sc));
+        memcpy(c.si, c.L.hsync + (reinterpret_cast<const double *>(c.L.si) - c.L.sc), sizeof(c.si));
+        memcpy(&c.status, c.L.hsync + (reinterpret_cast<const double *>(c.L.status) - c.L.sc), sizeof(int));
+        return c.status;
+    }
     cudaMemcpyAsync(c.sc, c.L.sc, sizeof(c.sc), cudaMemcpyDeviceToHost, c.s);
     cudaMemcpyAsync(c.si, c.L.si, sizeof(c.si), cudaMemcpyDeviceToHost, c.s);
     cudaMemcpyAsync(&c.status, c.L.status, sizeof(int), cudaMemcpyDeviceToHost, c.s);
@@ -995,7 +1105,7 @@ static int lg_state(LgCtx &c, int qv, int what) {
     const bool hess = what & SGP_EVAL_HESSIAN;
     const bool lik = mp.lik != SGP_LIK_QUADRATIC && (c.tau != 0.0 || (what & SGP_EVAL_SUMPOT));
     if (lik && !(what & SGP_EVAL_REUSE)) {
-        const int nb = 148;
+        const int nb = (mp.ld + LG_LIK_SPB - 1) / LG_LIK_SPB;
         k_lg_lik<<<nb, 256, 0, c.s>>>(c.L, c.L.vec + (size_t)qv * d);
         k_lg_lik_finish<<<1, 32, 0, c.s>>>(c.L, nb);
     } else if (!(what & SGP_EVAL_REUSE)) {
@@ -1012,30 +1122,39 @@ static int lg_state(LgCtx &c, int qv, int what) {
             const int fields[3] = {F_D2_00, F_D2_01, F_D2_11};
             // the J(J+1)/2 likelihood blocks in one batched launch (each 1040 x 1040 block alone
             // fills about half a wave of the GPU at C4)
-            GemmArgs hd[3];
+            // diagonal blocks first (full K), then the off-diagonal block as two K halves (the
+            // second into hpart, added by k_lg_addt_block): at C4 595 64 x 64 tiles were 2.01 waves
+            // of 296 CTA slots; 884 tiles with half-length off-diagonal ones fill ~3 waves
+            GemmArgs hd[4];
             int nbk = 0, maxM = 0, maxN = 0;
-            for (int j1 = 0; j1 < mp.J; ++j1)
-                for (int j2 = j1; j2 < mp.J; ++j2) {
-                    GemmArgs &g = hd[nbk++];
-                    g = GemmArgs{};
-                    g.M = mp.D[j1];
-                    g.N = mp.D[j2];
-                    g.K = mp.N;
-                    g.A = c.L.M.phis + (j1 ? mp.Dp0 : 0);
-                    g.lda = mp.Dp;
-                    g.TA = 1;
-                    g.B = c.L.M.phis + (j2 ? mp.Dp0 : 0);
-                    g.ldb = mp.Dp;
-                    g.scale = c.L.S + (size_t)fields[j1 + j2] * mp.ld;
-                    g.C = c.L.H + (size_t)mp.fstart[j1] * d + mp.fstart[j2];
-                    g.ldc = d;
-                    g.alpha = c.tau;
-                    g.upper_only = j1 == j2;
-                    g.a16 = (g.lda % 2 == 0) && ((reinterpret_cast<uintptr_t>(g.A) & 15) == 0);
-                    g.b16 = (g.ldb % 2 == 0) && ((reinterpret_cast<uintptr_t>(g.B) & 15) == 0);
-                    maxM = std::max(maxM, g.M);
-                    maxN = std::max(maxN, g.N);
-                }
+            const int kh = c.L.hpart ? ((mp.N / 2) & ~(GM_BK - 1)) : 0;
+            auto push = [&](int j1, int j2, int k0, int k1, double *C, int ldc) {
+                GemmArgs &g = hd[nbk++];
+                g = GemmArgs{};
+                g.M = mp.D[j1];
+                g.N = mp.D[j2];
+                g.K = k1 - k0;
+                g.A = c.L.M.phis + (size_t)k0 * mp.Dp + (j1 ? mp.Dp0 : 0);
+                g.lda = mp.Dp;
+                g.TA = 1;
+                g.B = c.L.M.phis + (size_t)k0 * mp.Dp + (j2 ? mp.Dp0 : 0);
+                g.ldb = mp.Dp;
+                g.scale = c.L.S + (size_t)fields[j1 + j2] * mp.ld + k0;
+                g.C = C;
+                g.ldc = ldc;
+                g.alpha = c.tau;
+                g.upper_only = j1 == j2;
+                g.a16 = (g.lda % 2 == 0) && ((reinterpret_cast<uintptr_t>(g.A) & 15) == 0);
+                g.b16 = (g.ldb % 2 == 0) && ((reinterpret_cast<uintptr_t>(g.B) & 15) == 0);
+                maxM = std::max(maxM, g.M);
+                maxN = std::max(maxN, g.N);
+            };
+            for (int j = 0; j < mp.J; ++j) push(j, j, 0, mp.N, c.L.H + (size_t)mp.fstart[j] * d + mp.fstart[j], d);
+            const bool split = mp.J == 2 && kh > 0;
+            if (mp.J == 2) {
+                push(0, 1, 0, split ? kh : mp.N, c.L.H + (size_t)mp.fstart[0] * d + mp.fstart[1], d);
+                if (split) push(0, 1, kh, mp.N, c.L.hpart, mp.D[1]);
+            }
             // all blocks share TA/TB; the alignment flags agree (same Phi buffer, same ld)
             cudaMemcpyAsync(c.L.hdesc, hd, sizeof(GemmArgs) * nbk, cudaMemcpyHostToDevice, c.s);
             gemm_launch_batched<1, 0>(c.L.hdesc, nbk, maxM, maxN, c.s);
@@ -1044,6 +1163,9 @@ static int lg_state(LgCtx &c, int qv, int what) {
                     if (j1 == j2)
                         k_lg_mirror_block<<<lg_blocks((size_t)mp.D[j1] * mp.D[j1]), 256, 0, c.s>>>(
                             c.L.H, d, mp.fstart[j1], mp.D[j1]);
+                    else if (split)
+                        k_lg_addt_block<<<dim3((mp.D[j2] + 31) / 32, (mp.D[j1] + 31) / 32), dim3(32, 8), 0, c.s>>>(
+                            c.L.H, d, mp.fstart[j1], mp.fstart[j2], mp.D[j1], mp.D[j2], c.L.hpart, mp.D[j2]);
                     else
                         k_lg_transpose_block<<<lg_blocks((size_t)mp.D[j1] * mp.D[j2]), 256, 0, c.s>>>(
                             c.L.H, d, mp.fstart[j1], mp.fstart[j2], mp.D[j1], mp.D[j2]);
@@ -1062,7 +1184,7 @@ static void lg_contraction(LgCtx &c, int slot, int pv) {
     k_lg_mmat<<<lg_blocks((size_t)d * d), 256, 0, c.s>>>(c.L, slot, c.cfg.kappa, -1.0, 1, 1);
     lg_gemm(c, d, d, d, c.L.P[slot], d, 0, c.L.W, d, 0, nullptr, c.L.X, d, 1.0, 0);  // X = Psi M
     lg_gemm(c, d, d, d, c.L.X, d, 0, c.L.P[slot], d, 1, nullptr, c.L.W, d, 1.0, 1);  // W = X Psi^T
-    k_mirror_upper<<<lg_blocks((size_t)d * d), 256, 0, c.s>>>(c.L.W, d, d);
+    mirror_upper(c.L.W, d, d, c.s);
 }
 
 // t (vec TV) = tr(W dH/dq) at vec[qv]; per-sample derivatives already in S
@@ -1325,7 +1447,8 @@ __global__ void k_cholqr_m(const double *G, int d, double *M, double *part) {
     double mx = 0.0;
     for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < (size_t)d * d;
          idx += (size_t)gridDim.x * blockDim.x) {
-        const int i = (int)(idx / d), j = (int)(idx - (size_t)i * d);
+        const unsigned u_ = (unsigned)idx;  // idx < d^2 < 2^32: 32-bit division
+        const int i = (int)(u_ / (unsigned)d), j = (int)(u_ - (unsigned)i * (unsigned)d);
         const double e = G[idx] - (i == j ? 1.0 : 0.0);
         mx = fmax(mx, fabs(e));
         M[idx] = (i == j) ? 1.0 - 0.5 * e : (i < j ? -e : 0.0);
@@ -1365,7 +1488,7 @@ static void lg_cholqr(LgCtx &c, int slot) {
     g.alpha = 1.0;
     g.upper_only = 1;
     gemm_launch(g, c.s);  // G = Psi^T Psi (upper tiles)
-    k_mirror_upper<<<lg_blocks(dd), 256, 0, c.s>>>(G, d, d);
+    mirror_upper(G, d, d, c.s);
     k_cholqr_m<<<148, 256, 0, c.s>>>(G, d, Mm, c.L.bjPart);
     k_max_final<<<1, 32, 0, c.s>>>(c.L.bjPart, 148, c.L.sc + 15);
     lg_sync(c);
@@ -1439,15 +1562,18 @@ __global__ void k_oa_E(const double *S, const double *G, const double *lam, int 
     double off2 = 0.0, mr = 0.0;
     for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < (size_t)d * d;
          idx += (size_t)gridDim.x * blockDim.x) {
-        const int i = (int)(idx / d), j = (int)(idx - (size_t)i * d);
+        const unsigned u_ = (unsigned)idx;  // idx < d^2 < 2^32: 32-bit division
+        const int i = (int)(u_ / (unsigned)d), j = (int)(u_ - (unsigned)i * (unsigned)d);
         if (i == j) {
             if (G) E[idx] = 0.5 * (1.0 - G[idx]);
             continue;
         }
-        const double sij = 0.5 * (S[idx] + S[(size_t)j * d + i]);
+        // S and G arrive mirrored from their upper triangles (k_mirror_upper), so
+        // 0.5 (s_ij + s_ji) == s_ij exactly: no strided transposed reads
+        const double sij = S[idx];
         off2 += sij * sij;
         if (G) {
-            const double rij = -0.5 * (G[idx] + G[(size_t)j * d + i]);
+            const double rij = -G[idx];
             if (fabs(sij) <= skip) {
                 // below the reference's skip threshold (|a_pq| <= tol/d, _jacobi.py:57-58): no
                 // rotation, only the orthogonality correction (Ogita-Aishima's clustered case)
@@ -1545,7 +1671,7 @@ static int lg_eig_refine(LgCtx &c, int src, int dst, int *sweeps) {
     for (int it = 0;; ++it) {
         lg_gemm_ab(c, d, d, d, c.L.H, d, 0, psi, d, 0, Y, d, 1.0, 0.0, 0);  // Y = H Psi
         lg_gemm_ab(c, d, d, d, psi, d, 1, Y, d, 0, Sm, d, 1.0, 0.0, 1);     // S = Psi^T Y (upper tiles)
-        k_mirror_upper<<<lg_blocks(dd), 256, 0, c.s>>>(Sm, d, d);
+        mirror_upper(Sm, d, d, c.s);
         k_oa_E<<<nb, 256, 0, c.s>>>(Sm, nullptr, nullptr, d, nullptr, c.L.bjPart);
         k_oa_fin<<<1, 32, 0, c.s>>>(c.L.bjPart, nb, c.L.sc + 13);
         lg_sync(c);
@@ -1578,7 +1704,7 @@ static int lg_eig_refine(LgCtx &c, int src, int dst, int *sweeps) {
         if (!(off < prev_off) || it >= std::min(c.cfg.sweep_cap, 8)) break;
         prev_off = off;
         lg_gemm_ab(c, d, d, d, psi, d, 1, psi, d, 0, G, d, 1.0, 0.0, 1);  // G = Psi^T Psi (upper tiles)
-        k_mirror_upper<<<lg_blocks(dd), 256, 0, c.s>>>(G, d, d);
+        mirror_upper(G, d, d, c.s);
         k_oa_lam<<<lg_blocks(d), 256, 0, c.s>>>(Sm, G, d, lam);
         int *pairs = c.L.jpairs, *npairs = c.L.jpairs + 2 * OA_MAXPAIRS;
         cudaMemsetAsync(npairs, 0, sizeof(int), c.s);
@@ -1734,12 +1860,12 @@ static int lg_alloc(const ModelDev &M, LgPtrs &L, void **owner) {
         off += (n + 3) & ~size_t(3);
         return o;
     };
-    const size_t oS = take((size_t)F_COUNT * ld), oH = take(dd), oX = take(dd), oW = take(dd), oP0 = take(dd),
+    const size_t oS = take((size_t)F_COUNT * ld), oH = take(dd), oX = take(std::max(dd, (size_t)LG_TV_KS * d))  /* also the Psi^T v partials */, oW = take(dd), oP0 = take(dd),
                  oP1 = take(dd), oY = take((size_t)std::max(M.mp.N, 1) * std::max(M.mp.Dtot, 1)),
                  osa = take(3 * (size_t)ld), ov = take(16 * (size_t)d), osc = take(16), osi = take(16),
                  ost = take(2), ojl = take(sgp_jacobi_log_doubles(d)), ojp = take(5 * np), ojq = take(std::max(2 * np, (size_t)4096)),  // + refine pair/cluster lists
                 
-                 ored = take(64);
+                 ored = take(std::max<size_t>(64, 2 * (size_t)((ld + 31) / 32) + 8));  // k_lg_lik partials
     // block Jacobi
     const int nbk = ((d + 2 * BJ_B - 1) / (2 * BJ_B)) * 2, dp = nbk * BJ_B, bnp = nbk / 2;
     const size_t dpp = (size_t)dp * dp;
@@ -1748,7 +1874,8 @@ static int lg_alloc(const ModelDev &M, LgPtrs &L, void **owner) {
                  obC = take((size_t)bnp);
     const size_t ndesc = (size_t)(nbk - 1) * 4 * bnp;
     const size_t obD = take((ndesc * sizeof(GemmArgs) + sizeof(double) - 1) / sizeof(double) + 2);
-    const size_t ohD = take((3 * sizeof(GemmArgs) + sizeof(double) - 1) / sizeof(double) + 2);
+    const size_t ohD = take((4 * sizeof(GemmArgs) + sizeof(double) - 1) / sizeof(double) + 2);
+    const size_t ohp = take(M.mp.J == 2 ? (size_t)M.mp.D[0] * M.mp.D[1] : 0);
     double *base = nullptr;
     if (cudaMalloc(&base, off * sizeof(double)) != cudaSuccess) return SGP_ENOMEM;
     cudaMemset(base, 0, off * sizeof(double));
@@ -1781,6 +1908,7 @@ static int lg_alloc(const ModelDev &M, LgPtrs &L, void **owner) {
     L.bjCnt = reinterpret_cast<int *>(base + obC);
     L.bjDesc = reinterpret_cast<GemmArgs *>(base + ((obD + 1) & ~size_t(1)));  // 16-byte aligned
     L.hdesc = reinterpret_cast<GemmArgs *>(base + ((ohD + 1) & ~size_t(1)));
+    L.hpart = M.mp.J == 2 ? base + ohp : nullptr;
     {
         L.bj_hs = nullptr;
         for (cudaEvent_t &e : L.bj_ev) e = nullptr;
@@ -1801,6 +1929,7 @@ static int lg_alloc(const ModelDev &M, LgPtrs &L, void **owner) {
     }
     L.jb = new JbWS();
     L.dc = new DcWS();
+    if (cudaMallocHost(&L.hsync, sizeof(double) * 64) != cudaSuccess) L.hsync = nullptr;
     *owner = base;
     return SGP_OK;
 }
