@@ -326,8 +326,10 @@ struct ChainLaunch {
     int nt, per_sm;
     SmemPlan pl;
 };
-static ChainLaunch chain_launch(const sgp_model *m) {
+static ChainLaunch chain_launch(const sgp_model *m, const sgp_chain_config *cfg = nullptr) {
     int nt = m->dev.mp.d <= 64 ? 64 : 256;
+    // path="latency" at small d: one wide CTA per chain (few chains, each alone on an SM)
+    if (cfg && cfg->path == SGP_PATH_LATENCY) nt = 256;
     const char *env = getenv("SGP_CHAIN_THREADS");
     if (env) {
         int v = atoi(env);
@@ -994,7 +996,7 @@ static int launch_moves(const sgp_model *m, const sgp_chain_config *cfg, const s
         return lg_run_moves(*LW, cfg, st, moves, move_offset, d_z, d_logu, const_cast<sgp_move_records *>(rec),
                             S(stream));
     }
-    const ChainLaunch L = chain_launch(m);
+    const ChainLaunch L = chain_launch(m, cfg);
     const size_t spc = sgp_scratch_doubles(m);
     int rc;
 #define SGP_LAUNCH_MOVES(NT_, MB_)                                                                        \

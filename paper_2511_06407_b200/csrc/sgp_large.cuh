@@ -1839,8 +1839,11 @@ static int lg_leapfrog(LgCtx &c, int &f, int *fp_p, int *fp_q, double *sweep_sum
 // 78 / 24, parallel 75 / 4.3; at d = 34 one CTA is faster (2.7 ms).  Opt-in, because the two
 // paths agree with the reference to 1e-9 but not bit for bit with each other, and the default
 // keeps a chain's bits independent of the batch it runs in.
+// At d <= 64 path="latency" stays on the fused kernel with 256-thread CTAs instead
+// (chain_launch): C1 1.96 ms/leapfrog cyclic, 1.07 parallel, vs 4.6 / 3.1 on this path.
+#define LG_LATENCY_MIN_D 65
 static bool lg_route_latency(const ModelDev &M, const sgp_chain_config &cfg) {
-    return cfg.path == SGP_PATH_LATENCY && M.mp.lik != SGP_LIK_QUADRATIC;
+    return cfg.path == SGP_PATH_LATENCY && M.mp.lik != SGP_LIK_QUADRATIC && M.mp.d >= LG_LATENCY_MIN_D;
 }
 
 static bool lg_is_large(const ModelDev &M) {
