@@ -47,13 +47,15 @@ class ChainConfig:
 
     ``cold_order``: the cold eigensolver (static_eigendecompose: chain start, rejections,
     rung starts).  "cyclic" (default) is the reference's order, bit-identical at every d;
-    "parallel" selects the block Jacobi at d > 256.
+    "parallel" selects the block Jacobi at d > 256; "dc" Householder tridiagonalisation +
+    divide and conquer (large-d path; 30 ms at d = 2083 against 21 s for the reference order).
 
     ``path``: "auto" (default) runs one CTA per chain for d <= 256 (many chains at once) and
-    the whole-GPU large path above; "latency" runs every chain's leapfrogs on the whole GPU
-    (d = 163: 24 ms per leapfrog in the cyclic order vs 78 ms in one CTA), chains one after
-    the other.  Both agree with the reference; "auto" keeps a chain's bits independent of its
-    batch."""
+    the whole-GPU large path above; "latency" serves few chains fast: at d <= 64 one 256-thread
+    CTA per chain (C1: 2.0 ms per leapfrog cyclic, 1.1 parallel), above it every chain's
+    leapfrogs on the whole GPU (d = 163: 24 ms per leapfrog in the cyclic order vs 78 ms in one
+    CTA, 3 ms with warm_order="refine"), chains one after the other.  Both agree with the
+    reference; "auto" keeps a chain's bits independent of its batch."""
 
     epsilon: float = 0.001
     leapfrogs: int = 100
