@@ -1701,7 +1701,10 @@ static int lg_eig_refine(LgCtx &c, int src, int dst, int *sweeps) {
             return lg_sync(c);
         }
         // quadratic convergence or hand over: non-finite, not decreasing, or too many iterations
-        if (!(off < prev_off) || it >= std::min(c.cfg.sweep_cap, 8)) break;
+        // (SGP_REFINE_MAX_ITERS: test hook forcing the hand-over)
+        const char *mi = getenv("SGP_REFINE_MAX_ITERS");
+        const int max_it = mi ? atoi(mi) : 8;
+        if (!(off < prev_off) || it >= std::min(c.cfg.sweep_cap, max_it)) break;
         prev_off = off;
         lg_gemm_ab(c, d, d, d, psi, d, 1, psi, d, 0, G, d, 1.0, 0.0, 1);  // G = Psi^T Psi (upper tiles)
         mirror_upper(G, d, d, c.s);
@@ -1717,7 +1720,19 @@ static int lg_eig_refine(LgCtx &c, int src, int dst, int *sweeps) {
         lg_gemm_ab(c, d, d, d, psi, d, 0, E, d, 0, Pn, d, 1.0, 1.0, 0);  // Psi + Psi E
         k_lg_copy<<<lg_blocks(dd), 256, 0, c.s>>>(psi, Pn, dd);
     }
-    // fall back to the block Jacobi from the original basis on the symmetric Hessian
+    // hand over: a full decomposition of the symmetric Hessian by tridiagonalisation + divide
+    // and conquer (sgp_dc.cuh, ~30 ms at d = 2083), or with SGP_REFINE_FALLBACK=jacobi the block
+    // Jacobi from the original basis
+    const char *fb = getenv("SGP_REFINE_FALLBACK");
+    if (!(fb && strcmp(fb, "jacobi") == 0) && c.L.dc && d <= DC_NMAX) {
+        if (getenv("SGP_DEBUG_REFINE")) fprintf(stderr, "refine -> divide-and-conquer fallback\n");
+        if (dc_eigh(*c.L.dc, c.L.H, d, d, lam, c.L.P[dst], d, c.s)) return SGP_STATUS_JACOBI;
+        k_lg_set_diag<<<lg_blocks(d), 256, 0, c.s>>>(c.L.H, lam, d);
+        *sweeps = std::min(c.cfg.sweep_cap, 8) + 1;
+        lg_op(c, LG_GLAM, dst, 0, 0, 0);
+        c.since[dst] = 0;
+        return lg_sync(c);
+    }
     if (getenv("SGP_DEBUG_REFINE")) fprintf(stderr, "refine -> block Jacobi fallback\n");
     return lg_eig_warm_jacobi(c, src, dst, sweeps);
 }

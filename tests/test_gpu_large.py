@@ -193,3 +193,28 @@ def test_large_chain_with_dc_cold_starts_like_oracle(large_case):
     assert res.records[0].h_before == pytest.approx(ref.records[0].h_before, rel=1e-10)
     assert all(np.isfinite(r.h_after) for r in res.records)
     assert res.accept_count >= 2
+
+
+@pytest.mark.parametrize("fallback", ["dc", "jacobi"])
+def test_refine_hand_over_vs_oracle(large_case, monkeypatch, fallback):
+    """The refinement hands a warm call over when it stops converging (here forced after one
+    iteration): to the divide and conquer (default) or the block Jacobi.  The leapfrog still
+    follows the reference algorithm to the Jacobi tolerance."""
+    monkeypatch.setenv("SGP_REFINE_MAX_ITERS", "1")
+    monkeypatch.setenv("SGP_REFINE_FALLBACK", fallback)
+    model, data, target, ot = large_case
+    d = target.dim
+    q0 = np.zeros(d)
+    om0 = oracle.metric_cold(ot.at(q0).hessian(), 1.0, 1e-13)
+    m0 = M.MetricState(eigenvalues=om0.lam, vectors=om0.psi, softabs_values=om0.g, logdet=om0.logdet,
+                       kappa=1.0, sweep_count=om0.sweeps, steps_since_refresh=0)
+    p = om0.psi @ (np.sqrt(om0.g) * np.random.default_rng(9).standard_normal(d))
+    cfg = S.ChainConfig(epsilon=0.002, leapfrogs=1, moves=1, burnin=0, warm_order="refine")
+    q1, p1, mt, diag = S.leapfrog_step(q0, p, m0, target, cfg)
+    oq, op_, om, odiag = oracle.leapfrog_step(q0, p, om0, ot, oracle.OConfig(epsilon=0.002, leapfrogs=1,
+                                                                             moves=1, burnin=0))
+    assert rel_err(q1, oq) < 1e-6
+    assert rel_err(p1, op_) < 1e-6
+    assert rel_err(np.sort(mt.eigenvalues), np.sort(om.lam)) < 1e-6
+    assert diag["fp_p_iters"] == odiag["fp_p_iters"]
+    assert diag["fp_q_iters"] == odiag["fp_q_iters"]
