@@ -16,6 +16,7 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #define GM_BK 32
 
@@ -183,32 +184,24 @@ __device__ __forceinline__ void gm_issue(const GemmArgs &g, double *st, int m0, 
     asm volatile("cp.async.commit_group;\n" ::);
 }
 
+// The cp.async pipeline over k-tiles [kt0, kt1) of output tile (tm, tn), accumulated into acc.
 template <int TA, int TB, class CFG>
-__device__ __forceinline__ void gm_body(const GemmArgs &g) {
+__device__ __forceinline__ void gm_accum(const GemmArgs &g, int tm, int tn, int kt0, int kt1, double *gsm,
+                                         double (&acc)[GmGeo<CFG>::FI][GmGeo<CFG>::FJ][2]) {
     using T = GmTile<TA, TB, CFG>;
     constexpr int GM_BM = CFG::BM, GM_BN = CFG::BN, GM_STAGES = CFG::STAGES;
     constexpr int GM_WARPS_N = CFG::WARPS_N, GM_WARPS_M = CFG::WARPS_M;
     constexpr int GM_FI = GmGeo<CFG>::FI, GM_FJ = GmGeo<CFG>::FJ;
-    const int tm = blockIdx.y, tn = blockIdx.x;
-    // symmetric outputs: skip tiles entirely below the diagonal (mirrored afterwards)
-    if (g.upper_only && tm * GM_BM > tn * GM_BN + GM_BN - 1) return;
-    if (tm * GM_BM >= g.M || tn * GM_BN >= g.N) return;  // batched launches size the grid for the largest
-    extern __shared__ __align__(16) double gsm[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int wm = (warp / GM_WARPS_N) * (GM_BM / GM_WARPS_M), wn = (warp % GM_WARPS_N) * (GM_BN / GM_WARPS_N);
     const int gid = lane >> 2, tig = lane & 3;
     const int m0 = tm * GM_BM, n0 = tn * GM_BN;
     const bool has_scale = g.scale != nullptr;
-    double acc[GM_FI][GM_FJ][2];
-#pragma unroll
-    for (int i = 0; i < GM_FI; ++i)
-#pragma unroll
-        for (int j = 0; j < GM_FJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-    const int nk = (g.K + GM_BK - 1) / GM_BK;
+    const int nk = kt1 - kt0;
 #pragma unroll
     for (int s = 0; s < GM_STAGES - 1; ++s) {
         if (s < nk)
-            gm_issue<TA, TB, CFG>(g, gsm + s * T::STAGE, m0, n0, s * GM_BK);
+            gm_issue<TA, TB, CFG>(g, gsm + s * T::STAGE, m0, n0, (kt0 + s) * GM_BK);
         else
             asm volatile("cp.async.commit_group;\n" ::);
     }
@@ -217,7 +210,7 @@ __device__ __forceinline__ void gm_body(const GemmArgs &g) {
         __syncthreads();
         const int nxt = kt + GM_STAGES - 1;
         if (nxt < nk)
-            gm_issue<TA, TB, CFG>(g, gsm + (nxt % GM_STAGES) * T::STAGE, m0, n0, nxt * GM_BK);
+            gm_issue<TA, TB, CFG>(g, gsm + (nxt % GM_STAGES) * T::STAGE, m0, n0, (kt0 + nxt) * GM_BK);
         else
             asm volatile("cp.async.commit_group;\n" ::);
         const double *As = gsm + (kt % GM_STAGES) * T::STAGE;
@@ -248,7 +241,20 @@ __device__ __forceinline__ void gm_body(const GemmArgs &g) {
         }
     }
     asm volatile("cp.async.wait_group 0;\n" ::);
-    // epilogue: C fragment (row gid, cols 2*tig, 2*tig+1)
+    __syncthreads();  // the stages may be refilled by the caller's next tile
+}
+
+// C fragment (row gid, cols 2*tig, 2*tig+1) of tile (tm, tn): alpha acc + beta C
+template <int TA, int TB, class CFG>
+__device__ __forceinline__ void gm_epilogue(const GemmArgs &g, int tm, int tn,
+                                            const double (&acc)[GmGeo<CFG>::FI][GmGeo<CFG>::FJ][2]) {
+    constexpr int GM_BM = CFG::BM, GM_BN = CFG::BN;
+    constexpr int GM_WARPS_N = CFG::WARPS_N, GM_WARPS_M = CFG::WARPS_M;
+    constexpr int GM_FI = GmGeo<CFG>::FI, GM_FJ = GmGeo<CFG>::FJ;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wm = (warp / GM_WARPS_N) * (GM_BM / GM_WARPS_M), wn = (warp % GM_WARPS_N) * (GM_BN / GM_WARPS_N);
+    const int gid = lane >> 2, tig = lane & 3;
+    const int m0 = tm * GM_BM, n0 = tn * GM_BN;
 #pragma unroll
     for (int i = 0; i < GM_FI; ++i) {
         const int m = m0 + wm + i * 8 + gid;
@@ -271,6 +277,95 @@ __device__ __forceinline__ void gm_body(const GemmArgs &g) {
                 *cp = v;
             }
         }
+    }
+}
+
+template <int TA, int TB, class CFG>
+__device__ __forceinline__ void gm_body(const GemmArgs &g) {
+    constexpr int GM_BM = CFG::BM, GM_BN = CFG::BN;
+    const int tm = blockIdx.y, tn = blockIdx.x;
+    // symmetric outputs: skip tiles entirely below the diagonal (mirrored afterwards)
+    if (g.upper_only && tm * GM_BM > tn * GM_BN + GM_BN - 1) return;
+    if (tm * GM_BM >= g.M || tn * GM_BN >= g.N) return;  // batched launches size the grid for the largest
+    extern __shared__ __align__(16) double gsm[];
+    double acc[GmGeo<CFG>::FI][GmGeo<CFG>::FJ][2];
+#pragma unroll
+    for (int i = 0; i < GmGeo<CFG>::FI; ++i)
+#pragma unroll
+        for (int j = 0; j < GmGeo<CFG>::FJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    gm_accum<TA, TB, CFG>(g, tm, tn, 0, (g.K + GM_BK - 1) / GM_BK, gsm, acc);
+    gm_epilogue<TA, TB, CFG>(g, tm, tn, acc);
+}
+
+// Stream-K (full outputs only): a persistent grid of co-resident CTAs splits the
+// tiles_m x tiles_n x nkt k-iterations evenly.  A CTA's range is the tail of a tile, whole tiles,
+// then the head of a tile.  Tails and middles go to the workspace (one slot per CTA: its first
+// work item is the only one that can be a non-head segment); the CTA holding a tile's head adds
+// the later segments' partials in k order (deterministic) after their flags carry this launch's
+// epoch, then writes the tile.  Removes the partial last wave of tile-parallel launches.
+__device__ __forceinline__ unsigned gm_ld_acquire(const unsigned *p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+template <int TA, int TB, class CFG>
+__global__ void __launch_bounds__(GmGeo<CFG>::THREADS) k_gemm_dmma_sk(GemmArgs g, int tiles_n, int nkt, long total,
+                                                                      double *ws, unsigned *flags, unsigned epoch) {
+    constexpr int FI = GmGeo<CFG>::FI, FJ = GmGeo<CFG>::FJ, NT = GmGeo<CFG>::THREADS;
+    constexpr int NACC = FI * FJ * 2;
+    extern __shared__ __align__(16) double gsm[];
+    const long per = (total + gridDim.x - 1) / gridDim.x;
+    const long it0 = (long)blockIdx.x * per, it1 = min(total, it0 + per);
+    long it = it0;
+    double acc[FI][FJ][2];
+    while (it < it1) {
+        const long tile = it / nkt;
+        const int kt0 = (int)(it - tile * nkt);
+        const int kt1 = (int)min((long)nkt, (long)kt0 + (it1 - it));
+        const int tm = (int)(tile / tiles_n), tn = (int)(tile - (long)tm * tiles_n);
+#pragma unroll
+        for (int i = 0; i < FI; ++i)
+#pragma unroll
+            for (int j = 0; j < FJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+        gm_accum<TA, TB, CFG>(g, tm, tn, kt0, kt1, gsm, acc);
+        if (kt0 != 0) {
+            // tail or middle segment: publish the partial for the tile's head CTA
+            double *slot = ws + (size_t)blockIdx.x * NACC * NT;
+#pragma unroll
+            for (int i = 0; i < FI; ++i)
+#pragma unroll
+                for (int j = 0; j < FJ; ++j)
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) __stcg(slot + ((i * FJ + j) * 2 + h) * NT + threadIdx.x, acc[i][j][h]);
+            __threadfence();
+            __syncthreads();
+            if (threadIdx.x == 0) atomicExch(flags + blockIdx.x, epoch);
+        } else {
+            // head segment: add the later segments in k order, then write the tile
+            long nit = it + (kt1 - kt0);
+            int kt = kt1;
+            while (kt < nkt) {
+                const int owner = (int)(nit / per);
+                if (threadIdx.x == 0)
+                    while (gm_ld_acquire(flags + owner) != epoch) {
+                    }
+                __syncthreads();
+                const double *slot = ws + (size_t)owner * NACC * NT;
+#pragma unroll
+                for (int i = 0; i < FI; ++i)
+#pragma unroll
+                    for (int j = 0; j < FJ; ++j)
+#pragma unroll
+                        for (int h = 0; h < 2; ++h)
+                            acc[i][j][h] += __ldcg(slot + ((i * FJ + j) * 2 + h) * NT + threadIdx.x);
+                const long oend = min(total, (long)(owner + 1) * per);
+                const int seg = (int)min((long)(nkt - kt), oend - nit);
+                kt += seg;
+                nit += seg;
+            }
+            gm_epilogue<TA, TB, CFG>(g, tm, tn, acc);
+        }
+        it += kt1 - kt0;
     }
 }
 
@@ -338,10 +433,100 @@ static inline long gemm_tiles(const GemmArgs &g) {
 // d^3 at d = 2083 28.8 vs 25.1 TF/s; the 1040 x 1040 Hessian blocks, 153 big tiles, stay small).
 static inline bool gemm_big_tiles(const GemmArgs &g) { return gemm_tiles<GmBig>(g) >= 250; }
 
+// Stream-K launch of a full big-tile GEMM when tile-parallel waves would waste more than 3 %
+// (C4: d^3 at d = 2083 561 tiles = 1.90 waves of 296 CTA slots, the trace 2112 = 7.14 waves).
+// Workspace (partials + flags) per (device, stream); SGP_GEMM_STREAMK=0 disables.
+struct GmSkWS {
+    int dev = -1;
+    cudaStream_t stream = nullptr;
+    double *ws = nullptr;
+    unsigned *flags = nullptr;
+    unsigned epoch = 0;
+    int grid = 0;
+};
+template <int TA, int TB>
+static inline bool gemm_launch_sk(const GemmArgs &g, cudaStream_t s, cudaError_t &err) {
+    using CFG = GmBig;
+    using T = GmTile<TA, TB, CFG>;
+    static const bool enabled = !(getenv("SGP_GEMM_STREAMK") && getenv("SGP_GEMM_STREAMK")[0] == '0');
+    if (!enabled || g.upper_only || g.ksplit || g.C2 || g.K <= 0) return false;
+    static bool configured = false;
+    static int per_sm = 0, sms = 0;
+    if (!configured) {
+        if (cudaFuncSetAttribute(k_gemm_dmma_sk<TA, TB, CFG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)T::SMEM) != cudaSuccess)
+            return false;
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gemm_dmma_sk<TA, TB, CFG>,
+                                                          GmGeo<CFG>::THREADS, T::SMEM) != cudaSuccess)
+            per_sm = 0;
+        configured = true;
+    }
+    if (per_sm < 1) return false;
+    const int slots = per_sm * sms;
+    const int tiles_m = (g.M + CFG::BM - 1) / CFG::BM, tiles_n = (g.N + CFG::BN - 1) / CFG::BN;
+    const long tiles = (long)tiles_m * tiles_n;
+    if (tiles < slots) return false;
+    const long waves = (tiles + slots - 1) / slots;
+    if ((double)tiles / (double)(waves * slots) >= 0.97) return false;
+    static GmSkWS cache[8];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    GmSkWS *w = nullptr;
+    for (GmSkWS &c : cache)
+        if (c.ws && c.dev == dev && c.stream == s) w = &c;
+    if (!w) {
+        for (GmSkWS &c : cache)
+            if (!c.ws) {
+                w = &c;
+                break;
+            }
+        if (!w) return false;
+        const size_t nacc = (size_t)GmGeo<CFG>::FI * GmGeo<CFG>::FJ * 2 * GmGeo<CFG>::THREADS;
+        if (cudaMalloc(&w->ws, sizeof(double) * nacc * slots) != cudaSuccess) {
+            w->ws = nullptr;
+            return false;
+        }
+        if (cudaMalloc(&w->flags, sizeof(unsigned) * slots) != cudaSuccess ||
+            cudaMemset(w->flags, 0, sizeof(unsigned) * slots) != cudaSuccess) {
+            cudaFree(w->ws);
+            w->ws = nullptr;
+            return false;
+        }
+        w->dev = dev;
+        w->stream = s;
+        w->grid = slots;
+    }
+    unsigned epoch = ++w->epoch;
+    if (epoch == 0) epoch = ++w->epoch;  // 0 is the flags' initial value
+    const int nkt = (g.K + GM_BK - 1) / GM_BK;
+    long total = tiles * nkt;
+    GemmArgs ga = g;
+    int tn = tiles_n, nk = nkt;
+    double *ws = w->ws;
+    unsigned *flags = w->flags;
+    void *args[] = {&ga, &tn, &nk, &total, &ws, &flags, &epoch};
+    err = cudaLaunchCooperativeKernel((void *)k_gemm_dmma_sk<TA, TB, CFG>, w->grid, GmGeo<CFG>::THREADS, args,
+                                      T::SMEM, s);
+    return err == cudaSuccess;
+}
+
 static inline cudaError_t gemm_launch(GemmArgs g, cudaStream_t s) {
     g.a16 = (g.lda % 2 == 0) && ((reinterpret_cast<uintptr_t>(g.A) & 15) == 0);
     g.b16 = (g.ldb % 2 == 0) && ((reinterpret_cast<uintptr_t>(g.B) & 15) == 0);
     const bool big = gemm_big_tiles(g) && !g.ksplit && !g.C2;
+    if (big) {
+        cudaError_t err = cudaSuccess;
+        bool done;
+        if (g.TA)
+            done = g.TB ? gemm_launch_sk<1, 1>(g, s, err) : gemm_launch_sk<1, 0>(g, s, err);
+        else
+            done = g.TB ? gemm_launch_sk<0, 1>(g, s, err) : gemm_launch_sk<0, 0>(g, s, err);
+        if (done) return err;
+        if (err != cudaSuccess) cudaGetLastError();  // a refused cooperative launch: tile-parallel instead
+    }
     if (g.TA) {
         if (g.TB) return big ? gemm_launch_t<1, 1, GmBig>(g, s) : gemm_launch_t<1, 1, GmSmall>(g, s);
         return big ? gemm_launch_t<1, 0, GmBig>(g, s) : gemm_launch_t<1, 0, GmSmall>(g, s);

@@ -114,6 +114,44 @@ int main() {
         printf("odd ld max err %.3e\n", err);
         fails += err > 1e-12;
     }
+    // stream-K path (full big-tile GEMM with a partial last wave: 11 x 32 = 352 tiles), all
+    // transposes, per-k scale and beta = 1
+    for (int ta = 0; ta < 2; ++ta)
+        for (int tb = 0; tb < 2; ++tb) {
+            int M = 1300, N = 2000, K = 200;
+            GemmArgs g{};
+            g.M = M; g.N = N; g.K = K; g.TA = ta; g.TB = tb;
+            g.lda = ((ta ? M : K) + 3) & ~3; g.ldb = ((tb ? K : N) + 3) & ~3; g.ldc = (N + 3) & ~3;
+            g.alpha = 0.7; g.beta = 1.0;
+            std::vector<double> A((size_t)(ta ? K : M) * g.lda), B((size_t)(tb ? N : K) * g.ldb), S(K),
+                C0((size_t)M * g.ldc), R((size_t)M * g.ldc), C((size_t)M * g.ldc);
+            for (auto &v : A) v = rand() / (double)RAND_MAX - 0.5;
+            for (auto &v : B) v = rand() / (double)RAND_MAX - 0.5;
+            for (auto &v : S) v = rand() / (double)RAND_MAX;
+            for (auto &v : C0) v = rand() / (double)RAND_MAX - 0.5;
+            double *dA, *dB, *dC, *dS;
+            cudaMalloc(&dA, A.size() * 8); cudaMalloc(&dB, B.size() * 8); cudaMalloc(&dC, C.size() * 8);
+            cudaMalloc(&dS, K * 8);
+            cudaMemcpy(dA, A.data(), A.size() * 8, cudaMemcpyHostToDevice);
+            cudaMemcpy(dB, B.data(), B.size() * 8, cudaMemcpyHostToDevice);
+            cudaMemcpy(dS, S.data(), K * 8, cudaMemcpyHostToDevice);
+            cudaMemcpy(dC, C0.data(), C0.size() * 8, cudaMemcpyHostToDevice);
+            g.A = dA; g.B = dB; g.C = dC; g.scale = dS;
+            cudaError_t e = gemm_launch(g, 0);
+            cudaDeviceSynchronize();
+            cudaMemcpy(C.data(), dC, C.size() * 8, cudaMemcpyDeviceToHost);
+            GemmArgs gr = g; gr.alpha = 1.0; gr.beta = 0.0;
+            ref(gr, A, B, S, R);
+            double err = 0;
+            for (int m = 0; m < M; ++m)
+                for (int n = 0; n < N; ++n) {
+                    const size_t i = (size_t)m * g.ldc + n;
+                    err = std::max(err, std::fabs(C[i] - (0.7 * R[i] + C0[i])));
+                }
+            printf("stream-K TA=%d TB=%d (launch %s) max err %.3e\n", ta, tb, cudaGetErrorString(e), err);
+            fails += err > 1e-12 || e != cudaSuccess;
+            cudaFree(dA); cudaFree(dB); cudaFree(dC); cudaFree(dS);
+        }
     // throughput
     struct Case { const char *name; int M, N, K, ta, tb, sc; } cases[] = {
         {"d^3 NN 2083", 2083, 2083, 2083, 0, 0, 0},
