@@ -824,12 +824,15 @@ extern "C" int sgp_chain_init(const sgp_model *m, const sgp_chain_config *cfg, c
 // sampler.py:322-328), `moves` moves run with the rung's draws (dz/dlogu indexed by rung), and
 // values[z * n_rungs + s] = log_likelihood at the rung's end (posterior.py:277-279), or its
 // average over the rung's moves when rung_average.  Per-move records are optional then.
-template <int NT, int MINB>
+// LADDER = false compiles the plain move loop without the rung machinery (its code shape
+// otherwise costs the register-capped 256-thread instance ~11 %: C5 2437 vs 2708/s).
+template <int NT, int MINB, bool LADDER>
 __global__ void __launch_bounds__(NT, MINB) k_run_moves(ModelDev M, SmemPlan pl, sgp_chain_config cfg,
                                                       sgp_chain_state st, int moves, int move_offset,
                                                       const double *dz, const double *dlogu, sgp_move_records rec,
-                                                      size_t spc, int n_rungs, const double *taus,
+                                                      size_t spc, int n_rungs_arg, const double *taus,
                                                       int rung_average, double *values) {
+    const int n_rungs = LADDER ? n_rungs_arg : 0;
     const int z = blockIdx.x;
     const int Z = st.n_chains;
     const int d = M.mp.d;
@@ -999,11 +1002,17 @@ static int launch_moves(const sgp_model *m, const sgp_chain_config *cfg, const s
     const ChainLaunch L = chain_launch(m, cfg);
     const size_t spc = sgp_scratch_doubles(m);
     int rc;
-#define SGP_LAUNCH_MOVES(NT_, MB_)                                                                        \
-    rc = launch_prep(k_run_moves<NT_, MB_>, L.pl.bytes);                                                 \
-    if (rc) return rc;                                                                                    \
-    k_run_moves<NT_, MB_><<<st->n_chains, NT_, L.pl.bytes, S(stream)>>>(                                   \
+#define SGP_LAUNCH_MOVES_L(NT_, MB_, LD_)                                                                   \
+    rc = launch_prep(k_run_moves<NT_, MB_, LD_>, L.pl.bytes);                                              \
+    if (rc) return rc;                                                                                      \
+    k_run_moves<NT_, MB_, LD_><<<st->n_chains, NT_, L.pl.bytes, S(stream)>>>(                                \
         m->dev, L.pl, *cfg, *st, moves, move_offset, d_z, d_logu, *rec, spc, n_rungs, d_taus, rung_average, d_values)
+#define SGP_LAUNCH_MOVES(NT_, MB_)              \
+    if (n_rungs > 0) {                          \
+        SGP_LAUNCH_MOVES_L(NT_, MB_, true);     \
+    } else {                                    \
+        SGP_LAUNCH_MOVES_L(NT_, MB_, false);    \
+    }
     if (L.nt == 32) {
         SGP_LAUNCH_MOVES(32, 12);
     } else if (L.nt == 64) {
@@ -1020,6 +1029,7 @@ static int launch_moves(const sgp_model *m, const sgp_chain_config *cfg, const s
         SGP_LAUNCH_MOVES(256, 2);
     }
 #undef SGP_LAUNCH_MOVES
+#undef SGP_LAUNCH_MOVES_L
     return check_launch();
 }
 
