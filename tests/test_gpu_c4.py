@@ -150,3 +150,21 @@ def test_c4_refine_leapfrog_matches_reference(c4, c4_start):
     assert [diag["fp_p_iters"]] == list(g["fp_p1"])
     assert [diag["fp_q_iters"]] == list(g["fp_q1"])
     assert all(0 < s <= 4 for s in diag["sweeps"])
+
+
+def test_c4_divide_and_conquer_cold_matches_reference(c4_start):
+    """cold_order="dc" on the real chain-start Hessian (north star (3)): the reference's cold
+    spectrum (golden, its own Jacobi) to 1e-12, a 1e-12 decomposition residual, an orthonormal
+    basis, and the reference's metric log-determinant and starting Hamiltonian (basis-invariant)."""
+    g, q0, h0, _ = c4_start
+    lam, psi = M.eigh_dc(h0)
+    assert np.all(np.diff(lam) >= 0.0)
+    assert rel_err(lam, np.sort(g["cold_lam"])) < 1e-12
+    hs = 0.5 * (h0 + h0.T)
+    fro = np.linalg.norm(hs)
+    assert np.linalg.norm(psi @ (lam[:, None] * psi.T) - hs) < 1e-12 * fro
+    assert np.max(np.abs(psi.T @ psi - np.eye(D))) < 1e-12
+    m = M._state(lam, psi, 1.0, 0, 0)
+    assert m.logdet == pytest.approx(float(g["cold_logdet"]), rel=1e-12)
+    p = psi @ (np.sqrt(m.softabs_values) * g["z"])
+    assert S.hamiltonian(q0, p, m, c4_start_target()) == pytest.approx(float(g["h_before"]), rel=1e-12)
