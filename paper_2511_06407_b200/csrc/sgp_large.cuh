@@ -1551,6 +1551,7 @@ __global__ void k_oa_lam(const double *S, const double *G, int d, double *lam) {
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < d; i += gridDim.x * blockDim.x)
         lam[i] = S[(size_t)i * d + i] / G[(size_t)i * d + i];
 }
+#define OA_NB 592  // k_oa_E blocks (4 per SM): enough loads in flight for the d x d pass
 #define OA_ETA 1e3  // a coupling this far above its eigenvalue gap goes to the block Jacobi
 #define OA_MAXPAIRS 1024
 // off-norm^2 of sym(S) and E (when G is given); partials per CTA: [off2, max ratio of the
@@ -1617,13 +1618,21 @@ __global__ void k_oa_E(const double *S, const double *G, const double *lam, int 
         part[2 * blockIdx.x + 1] = b;
     }
 }
+// one warp: lanes take partials lane, lane+32, ... (fixed order), xor trees (sum; max with NaN
+// propagation) give every lane the same totals
 __global__ void k_oa_fin(const double *part, int n, double *out) {
-    if (threadIdx.x == 0 && blockIdx.x == 0) {
-        double a = 0.0, b = 0.0;
-        for (int i = 0; i < n; ++i) {
-            a += part[2 * i];
-            b = (part[2 * i + 1] > b || part[2 * i + 1] != part[2 * i + 1]) ? part[2 * i + 1] : b;
-        }
+    if (blockIdx.x != 0 || threadIdx.x >= 32) return;
+    double a = 0.0, b = 0.0;
+    for (int i = threadIdx.x; i < n; i += 32) {
+        a += part[2 * i];
+        b = (part[2 * i + 1] > b || part[2 * i + 1] != part[2 * i + 1]) ? part[2 * i + 1] : b;
+    }
+    for (int o = 16; o; o >>= 1) {
+        a += __shfl_xor_sync(0xffffffffu, a, o);
+        const double v = __shfl_xor_sync(0xffffffffu, b, o);
+        b = (v > b || v != v) ? v : b;
+    }
+    if (threadIdx.x == 0) {
         out[0] = sqrt(a);
         out[1] = b;
     }
@@ -1666,7 +1675,7 @@ static int lg_eig_refine(LgCtx &c, int src, int dst, int *sweeps) {
     double *psi = c.L.P[dst], *Y = c.L.X, *Sm = c.L.W, *G = c.L.bjA, *E = c.L.bjT, *Pn = c.L.bjV[0];
     double *lam = c.L.vec + (size_t)V_TMP * d;  // scratch d-vector (free during the eigensolver)
     k_lg_copy<<<lg_blocks(dd), 256, 0, c.s>>>(psi, c.L.P[src], dd);
-    const int nb = 148;  // two partials per CTA: bjPart holds 512 doubles
+    const int nb = OA_NB;  // two partials per CTA in bjPart
     double prev_off = INFINITY;
     for (int it = 0;; ++it) {
         lg_gemm_ab(c, d, d, d, c.L.H, d, 0, psi, d, 0, Y, d, 1.0, 0.0, 0);  // Y = H Psi
@@ -1888,7 +1897,7 @@ static int lg_alloc(const ModelDev &M, LgPtrs &L, void **owner) {
     const int nbk = ((d + 2 * BJ_B - 1) / (2 * BJ_B)) * 2, dp = nbk * BJ_B, bnp = nbk / 2;
     const size_t dpp = (size_t)dp * dp;
     const size_t obA = take(dpp), obT = take(dpp), obV0 = take(dpp), obV1 = take(dpp),
-                 obU = take((size_t)2 * bnp * BJ_N * BJ_N), obL = take((size_t)bnp * BJ_N * BJ_N), obP = take(512),
+                 obU = take((size_t)2 * bnp * BJ_N * BJ_N), obL = take((size_t)bnp * BJ_N * BJ_N), obP = take(2 * OA_NB + 8),
                  obC = take((size_t)bnp);
     const size_t ndesc = (size_t)(nbk - 1) * 4 * bnp;
     const size_t obD = take((ndesc * sizeof(GemmArgs) + sizeof(double) - 1) / sizeof(double) + 2);
