@@ -235,17 +235,31 @@ __global__ void k_lg_mmat(LgPtrs L, int slot, double kappa, double c1, int with_
     }
 }
 
-__global__ void k_lg_symmetrize(double *A, int d) {
-    for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < (size_t)d * d;
-         idx += (size_t)gridDim.x * blockDim.x) {
-        const unsigned u_ = (unsigned)idx;  // idx < d^2 < 2^32: 32-bit division
-        const int i = (int)(u_ / (unsigned)d), j = (int)(u_ - (unsigned)i * (unsigned)d);
-        if (i < j) {
-            const double v = 0.5 * (A[idx] + A[(size_t)j * d + i]);
-            A[idx] = v;
-            A[(size_t)j * d + i] = v;
-        }
+// A <- 0.5 (A + A^T): tile pairs (ti, tj), ti <= tj, through shared memory (both sides
+// coalesced).  Launch: grid (nt, nt), block (32, 8).
+__global__ void k_lg_symmetrize_tiled(double *A, int d) {
+    __shared__ double up[32][33], lo[32][33];
+    const int ti = blockIdx.y, tj = blockIdx.x;
+    if (ti > tj) return;
+    const int r0 = ti * 32, c0 = tj * 32;
+    for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+        const int r = r0 + k, c = c0 + threadIdx.x;
+        if (r < d && c < d) up[k][threadIdx.x] = A[(size_t)r * d + c];
+        const int r2 = c0 + k, c2 = r0 + threadIdx.x;
+        if (r2 < d && c2 < d) lo[k][threadIdx.x] = A[(size_t)r2 * d + c2];
     }
+    __syncthreads();
+    for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+        // upper element (r0+k, c0+x) pairs with lower (c0+x, r0+k) = lo[x][k]
+        const int r = r0 + k, c = c0 + threadIdx.x;
+        if (r < d && c < d && r < c) A[(size_t)r * d + c] = 0.5 * (up[k][threadIdx.x] + lo[threadIdx.x][k]);
+        const int r2 = c0 + k, c2 = r0 + threadIdx.x;
+        if (r2 < d && c2 < d && r2 > c2) A[(size_t)r2 * d + c2] = 0.5 * (up[threadIdx.x][k] + lo[k][threadIdx.x]);
+    }
+}
+static inline void lg_symmetrize(double *A, int d, cudaStream_t s) {
+    const int nt = (d + 31) / 32;
+    k_lg_symmetrize_tiled<<<dim3(nt, nt), dim3(32, 8), 0, s>>>(A, d);
 }
 
 __global__ void k_lg_copy(double *dst, const double *src, size_t n) {
@@ -1341,7 +1355,7 @@ static int lg_eig_cold(LgCtx &c, int dst, int *sweeps) {
         c.since[dst] = 0;
         return lg_sync(c);
     }
-    k_lg_symmetrize<<<lg_blocks((size_t)d * d), 256, 0, c.s>>>(c.L.H, d);
+    lg_symmetrize(c.L.H, d, c.s);
     const double hnorm = lg_hnorm(c);
     const double tol = c.cfg.zeta * hnorm, skip = d ? tol / d : 0.0;
     k_lg_eye<<<lg_blocks((size_t)d * d), 256, 0, c.s>>>(c.L.P[dst], d);
@@ -1671,7 +1685,7 @@ static int lg_eig_refine(LgCtx &c, int src, int dst, int *sweeps) {
     if (c.cfg.gs_interval && since >= c.cfg.gs_interval) since = 0;  // orthonormality is refined every iteration
     const double hnorm = lg_hnorm(c);  // ||H||_F of the unsymmetrised Hessian (metric.py:172)
     const double tol = c.cfg.zeta * hnorm;
-    k_lg_symmetrize<<<lg_blocks(dd), 256, 0, c.s>>>(c.L.H, d);
+    lg_symmetrize(c.L.H, d, c.s);
     double *psi = c.L.P[dst], *Y = c.L.X, *Sm = c.L.W, *G = c.L.bjA, *E = c.L.bjT, *Pn = c.L.bjV[0];
     double *lam = c.L.vec + (size_t)V_TMP * d;  // scratch d-vector (free during the eigensolver)
     k_lg_copy<<<lg_blocks(dd), 256, 0, c.s>>>(psi, c.L.P[src], dd);
@@ -1772,7 +1786,7 @@ static int lg_eig_warm_jacobi(LgCtx &c, int src, int dst, int *sweeps) {
     const double hnorm = lg_hnorm(c);
     lg_gemm(c, d, d, d, c.L.P[src], d, 1, c.L.H, d, 0, nullptr, c.L.X, d, 1.0, 0);  // X = Psi^T H
     lg_gemm(c, d, d, d, c.L.X, d, 0, c.L.P[src], d, 0, nullptr, c.L.H, d, 1.0, 0);  // A = X Psi
-    k_lg_symmetrize<<<lg_blocks((size_t)d * d), 256, 0, c.s>>>(c.L.H, d);
+    lg_symmetrize(c.L.H, d, c.s);
     k_lg_copy<<<lg_blocks((size_t)d * d), 256, 0, c.s>>>(c.L.P[dst], c.L.P[src], (size_t)d * d);
     const double tol = c.cfg.zeta * hnorm, skip = d ? tol / d : 0.0;
     const int st = lg_jacobi(c, dst, tol, skip, c.cfg.warm_order != SGP_ORDER_CYCLIC, sweeps);
@@ -2259,7 +2273,7 @@ static int lg_trace_api(const LgPtrs &L, int Z, const double *d_tau, const doubl
         int rc = lg_state(c, V_Q0, 0);
         if (!rc) {
             cudaMemcpyAsync(L.W, d_w + (size_t)z * d * d, sizeof(double) * d * d, cudaMemcpyDeviceToDevice, s);
-            k_lg_symmetrize<<<lg_blocks((size_t)d * d), 256, 0, s>>>(L.W, d);
+            lg_symmetrize(L.W, d, c.s);
             rc = lg_trace(c, V_Q0);
         }
         cudaMemcpyAsync(d_t + (size_t)z * d, L.vec + (size_t)V_TV * d, sizeof(double) * d, cudaMemcpyDeviceToDevice, s);
