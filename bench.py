@@ -425,6 +425,12 @@ def _dist_setup():
     return torch, dist, world, rank, dev_index
 
 
+def _reduce_device(dist):
+    """Device of the max-over-ranks reductions: CUDA tensors under NCCL (the measurement
+    backend), host tensors under gloo (functional multi-rank runs on a one-GPU box)."""
+    return "cuda" if dist.is_initialized() and dist.get_backend() == "nccl" else "cpu"
+
+
 def count_kernel_launches(torch, fn):
     """Kernels launched by fn() (CUPTI activity records through torch.profiler), untimed."""
     from torch.profiler import ProfilerActivity, profile
@@ -502,7 +508,8 @@ def run_gpu_c4(args):
         raise RuntimeError(f"chain stopped during the timed region (status {status}): no valid throughput")
     dev_s = sum(a.elapsed_time(b) for a, b in times) / 1e3
     acc = float(torch.stack(accepted).float().mean().item())
-    t_max = torch.tensor([dev_s], dtype=torch.float64, device="cuda")
+    t_max = torch.tensor([dev_s], dtype=torch.float64,
+                         device=_reduce_device(dist) if world > 1 else "cuda")
     if world > 1:
         dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
     T = float(t_max.item())
@@ -533,7 +540,8 @@ def run_gpu_c4(args):
         q_pin.copy_(chains.q, non_blocking=True)
         torch.cuda.synchronize()
     e2e_t = time.perf_counter() - t0
-    e2e_max = torch.tensor([e2e_t], dtype=torch.float64, device="cuda")
+    e2e_max = torch.tensor([e2e_t], dtype=torch.float64,
+                         device=_reduce_device(dist) if world > 1 else "cuda")
     if world > 1:
         dist.all_reduce(e2e_max, op=dist.ReduceOp.MAX)
     e2e_value = world * Z * C * e2e_steps / float(e2e_max.item())
@@ -677,7 +685,8 @@ def run_gpu_c5(args):
         t_wall = time.perf_counter() - t_wall
     bad = sum(int(np.count_nonzero(b["ch"].status_host())) for b in batches)
     dev_s = sum(a.elapsed_time(b) for a, b in times) / 1e3
-    t_max = torch.tensor([dev_s], dtype=torch.float64, device="cuda")
+    t_max = torch.tensor([dev_s], dtype=torch.float64,
+                         device=_reduce_device(dist) if world > 1 else "cuda")
     if world > 1:
         dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
     T = float(t_max.item())
@@ -703,7 +712,8 @@ def run_gpu_c5(args):
             d2h += len(b["zs"]) * (A * 7 + b["d"]) * 8
     torch.cuda.synchronize()
     e2e_t = time.perf_counter() - t0
-    e2e_max = torch.tensor([e2e_t], dtype=torch.float64, device="cuda")
+    e2e_max = torch.tensor([e2e_t], dtype=torch.float64,
+                         device=_reduce_device(dist) if world > 1 else "cuda")
     if world > 1:
         dist.all_reduce(e2e_max, op=dist.ReduceOp.MAX)
     e2e_value = n_units * A * C * e2e_steps / float(e2e_max.item())
@@ -819,7 +829,8 @@ def run_gpu(args):
     bufs = chains._rec[1]
     acc = float(bufs["accept"].float().mean().item())
     sweeps = float(bufs["sweeps_mean"].mean().item())
-    t_max = torch.tensor([dev_s], dtype=torch.float64, device="cuda")
+    t_max = torch.tensor([dev_s], dtype=torch.float64,
+                         device=_reduce_device(dist) if world > 1 else "cuda")
     if world > 1:
         dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
     T = float(t_max.item())
@@ -851,7 +862,8 @@ def run_gpu(args):
         q_pin.copy_(chains.q, non_blocking=True)
         torch.cuda.synchronize()
     e2e_t = time.perf_counter() - t0
-    e2e_max = torch.tensor([e2e_t], dtype=torch.float64, device="cuda")
+    e2e_max = torch.tensor([e2e_t], dtype=torch.float64,
+                         device=_reduce_device(dist) if world > 1 else "cuda")
     if world > 1:
         dist.all_reduce(e2e_max, op=dist.ReduceOp.MAX)
     e2e_value = world * Z * LEAPFROGS * e2e_steps / float(e2e_max.item())
