@@ -282,7 +282,8 @@ __global__ void k_lg_rowdot(LgPtrs L, int j1, int final_pass) {
         const double *y = L.Y + (size_t)i * Dt;
         const double *ph = L.M.phis + (size_t)i * mp.Dp;
         double s0 = 0.0, s1 = 0.0;
-        for (int b = lane; b < Dt; b += 32) {
+        // second block (J = 2): only its own columns were formed (s10 = s01, W symmetric)
+        for (int b = (j1 == 1 ? mp.D[0] : 0) + lane; b < Dt; b += 32) {
             const bool blk1 = b >= mp.D[0];
             const int pb = blk1 ? mp.Dp0 + (b - mp.D[0]) : b;
             const double v = y[b] * ph[pb];
@@ -300,7 +301,10 @@ __global__ void k_lg_rowdot(LgPtrs L, int j1, int final_pass) {
                 sa[ld + i] = s1;      // s01 (cross, first half)
                 sa[2 * ld + i] = 0.0;
             } else {
-                sa[ld + i] += s0;     // s10
+                // s01 + s10 with s10 = s01: W is exactly symmetric (mirrored), so
+                // phi_1^T W_10 phi_0 equals phi_0^T W_01 phi_1 up to rounding (posterior.py:495-509
+                // forms both)
+                sa[ld + i] += sa[ld + i];
                 sa[2 * ld + i] = s1;  // s11
             }
             if (final_pass) {
@@ -1209,7 +1213,11 @@ static int lg_trace(LgCtx &c, int qv) {
         for (int j1 = 0; j1 < mp.J; ++j1) {
             const double *a = c.L.M.phis + (j1 ? mp.Dp0 : 0);
             const double *b = c.L.W + (size_t)mp.fstart[j1] * d;
-            lg_gemm(c, mp.N, mp.Dtot, mp.D[j1], a, mp.Dp, 0, b, d, 0, nullptr, c.L.Y, mp.Dtot, 1.0, 0);
+            if (j1 == 1)  // Y_1 over block 1's columns only: the (1,0) block repeats (0,1) (W symmetric)
+                lg_gemm(c, mp.N, mp.D[1], mp.D[1], a, mp.Dp, 0, b + mp.fstart[1], d, 0, nullptr, c.L.Y + mp.D[0],
+                        mp.Dtot, 1.0, 0);
+            else
+                lg_gemm(c, mp.N, mp.Dtot, mp.D[j1], a, mp.Dp, 0, b, d, 0, nullptr, c.L.Y, mp.Dtot, 1.0, 0);
             k_lg_rowdot<<<lg_blocks((size_t)mp.N * 32), 256, 0, c.s>>>(c.L, j1, j1 == mp.J - 1);
         }
         k_lg_project<<<lg_blocks((size_t)mp.Dtot * 32), 256, 0, c.s>>>(c.L, c.tau, F_C0, F_C1,
