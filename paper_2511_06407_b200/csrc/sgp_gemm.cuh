@@ -17,6 +17,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdlib.h>
+#include <vector>
 
 #define GM_BK 32
 
@@ -433,6 +434,103 @@ static inline long gemm_tiles(const GemmArgs &g) {
 // d^3 at d = 2083 28.8 vs 25.1 TF/s; the 1040 x 1040 Hessian blocks, 153 big tiles, stay small).
 static inline bool gemm_big_tiles(const GemmArgs &g) { return gemm_tiles<GmBig>(g) >= 250; }
 
+// Grouped stream-K: several GEMMs (same TA/TB; descriptors in device memory) as one iteration
+// space.  tiles[t] = (descriptor, tm, tn, k-tiles), prefix[t] = k-iterations before tile t
+// (prefix[ntiles] = total); upper_only descriptors list only their computed tiles.  Same
+// partial/flag protocol as k_gemm_dmma_sk.
+template <int TA, int TB, class CFG>
+__global__ void __launch_bounds__(GmGeo<CFG>::THREADS)
+    k_gemm_dmma_skg(const GemmArgs *descs, const int4 *tiles, const long *prefix, int ntiles, double *ws,
+                    unsigned *flags, unsigned epoch) {
+    constexpr int FI = GmGeo<CFG>::FI, FJ = GmGeo<CFG>::FJ, NT = GmGeo<CFG>::THREADS;
+    constexpr int NACC = FI * FJ * 2;
+    extern __shared__ __align__(16) double gsm[];
+    const long total = prefix[ntiles];
+    const long per = (total + gridDim.x - 1) / gridDim.x;
+    const long it0 = (long)blockIdx.x * per, it1 = min(total, it0 + per);
+    if (it0 >= it1) return;
+    int t = 0;
+    {  // first tile with prefix[t + 1] > it0
+        int lo = 0, hi = ntiles - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (prefix[mid + 1] > it0)
+                hi = mid;
+            else
+                lo = mid + 1;
+        }
+        t = lo;
+    }
+    long it = it0;
+    double acc[FI][FJ][2];
+    while (it < it1) {
+        const int4 tl = tiles[t];
+        const GemmArgs g = descs[tl.x];
+        const int nkt = tl.w;
+        const int kt0 = (int)(it - prefix[t]);
+        const int kt1 = (int)min((long)nkt, (long)kt0 + (it1 - it));
+#pragma unroll
+        for (int i = 0; i < FI; ++i)
+#pragma unroll
+            for (int j = 0; j < FJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+        gm_accum<TA, TB, CFG>(g, tl.y, tl.z, kt0, kt1, gsm, acc);
+        if (kt0 != 0) {
+            double *slot = ws + (size_t)blockIdx.x * NACC * NT;
+#pragma unroll
+            for (int i = 0; i < FI; ++i)
+#pragma unroll
+                for (int j = 0; j < FJ; ++j)
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) __stcg(slot + ((i * FJ + j) * 2 + h) * NT + threadIdx.x, acc[i][j][h]);
+            __threadfence();
+            __syncthreads();
+            if (threadIdx.x == 0) atomicExch(flags + blockIdx.x, epoch);
+        } else {
+            long nit = it + (kt1 - kt0);
+            int kt = kt1;
+            while (kt < nkt) {
+                const int owner = (int)(nit / per);
+                if (threadIdx.x == 0)
+                    while (gm_ld_acquire(flags + owner) != epoch) {
+                    }
+                __syncthreads();
+                const double *slot = ws + (size_t)owner * NACC * NT;
+#pragma unroll
+                for (int i = 0; i < FI; ++i)
+#pragma unroll
+                    for (int j = 0; j < FJ; ++j)
+#pragma unroll
+                        for (int h = 0; h < 2; ++h)
+                            acc[i][j][h] += __ldcg(slot + ((i * FJ + j) * 2 + h) * NT + threadIdx.x);
+                const long oend = min(total, (long)(owner + 1) * per);
+                const int seg = (int)min((long)(nkt - kt), oend - nit);
+                kt += seg;
+                nit += seg;
+            }
+            gm_epilogue<TA, TB, CFG>(g, tl.y, tl.z, acc);
+        }
+        it += kt1 - kt0;
+        ++t;
+    }
+}
+
+// Tile list of a grouped GEMM (host): descriptors' shapes only.
+static inline void gemm_group_tiles(const GemmArgs *gs, int n, std::vector<int4> &tiles, std::vector<long> &prefix) {
+    tiles.clear();
+    prefix.assign(1, 0);
+    for (int di = 0; di < n; ++di) {
+        const GemmArgs &g = gs[di];
+        const int tm_n = (g.M + GmBig::BM - 1) / GmBig::BM, tn_n = (g.N + GmBig::BN - 1) / GmBig::BN;
+        const int nkt = (g.K + GM_BK - 1) / GM_BK;
+        for (int tm = 0; tm < tm_n; ++tm)
+            for (int tn = 0; tn < tn_n; ++tn) {
+                if (g.upper_only && tm * GmBig::BM > tn * GmBig::BN + GmBig::BN - 1) continue;
+                tiles.push_back(make_int4(di, tm, tn, nkt));
+                prefix.push_back(prefix.back() + nkt);
+            }
+    }
+}
+
 // Stream-K launch of a full big-tile GEMM when tile-parallel waves would waste more than 3 %
 // (C4: d^3 at d = 2083 561 tiles = 1.90 waves of 296 CTA slots, the trace 2112 = 7.14 waves).
 // Workspace (partials + flags) per (device, stream); SGP_GEMM_STREAMK=0 disables.
@@ -444,6 +542,76 @@ struct GmSkWS {
     unsigned epoch = 0;
     int grid = 0;
 };
+// partials + flags of the stream-K launches on stream s (one set per device and stream)
+static inline GmSkWS *gm_sk_ws(cudaStream_t s, int slots) {
+    static GmSkWS cache[8];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    for (GmSkWS &c : cache)
+        if (c.ws && c.dev == dev && c.stream == s) return c.grid >= slots ? &c : nullptr;
+    GmSkWS *w = nullptr;
+    for (GmSkWS &c : cache)
+        if (!c.ws) {
+            w = &c;
+            break;
+        }
+    if (!w) return nullptr;
+    const size_t nacc = (size_t)GmGeo<GmBig>::FI * GmGeo<GmBig>::FJ * 2 * GmGeo<GmBig>::THREADS;
+    if (cudaMalloc(&w->ws, sizeof(double) * nacc * slots) != cudaSuccess) {
+        w->ws = nullptr;
+        return nullptr;
+    }
+    if (cudaMalloc(&w->flags, sizeof(unsigned) * slots) != cudaSuccess ||
+        cudaMemset(w->flags, 0, sizeof(unsigned) * slots) != cudaSuccess) {
+        cudaFree(w->ws);
+        w->ws = nullptr;
+        return nullptr;
+    }
+    w->dev = dev;
+    w->stream = s;
+    w->grid = slots;
+    return w;
+}
+
+// Grouped stream-K launch (descriptors and tile list in device memory); false if unavailable.
+template <int TA, int TB>
+static inline bool gemm_launch_skg(const GemmArgs *d_descs, const int4 *d_tiles, const long *d_prefix, int ntiles,
+                                   cudaStream_t s) {
+    using CFG = GmBig;
+    using T = GmTile<TA, TB, CFG>;
+    static bool configured = false;
+    static int per_sm = 0, sms = 0;
+    if (!configured) {
+        if (cudaFuncSetAttribute(k_gemm_dmma_skg<TA, TB, CFG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)T::SMEM) != cudaSuccess)
+            return false;
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gemm_dmma_skg<TA, TB, CFG>,
+                                                          GmGeo<CFG>::THREADS, T::SMEM) != cudaSuccess)
+            per_sm = 0;
+        configured = true;
+    }
+    if (per_sm < 1 || ntiles < 1) return false;
+    const int slots = per_sm * sms;
+    GmSkWS *w = gm_sk_ws(s, slots);
+    if (!w) return false;
+    unsigned epoch = ++w->epoch;
+    if (epoch == 0) epoch = ++w->epoch;
+    double *ws = w->ws;
+    unsigned *flags = w->flags;
+    int nt = ntiles;
+    void *args[] = {(void *)&d_descs, (void *)&d_tiles, (void *)&d_prefix, &nt, &ws, &flags, &epoch};
+    const cudaError_t err = cudaLaunchCooperativeKernel((void *)k_gemm_dmma_skg<TA, TB, CFG>, slots,
+                                                        GmGeo<CFG>::THREADS, args, T::SMEM, s);
+    if (err != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return true;
+}
+
 template <int TA, int TB>
 static inline bool gemm_launch_sk(const GemmArgs &g, cudaStream_t s, cudaError_t &err) {
     using CFG = GmBig;
@@ -471,34 +639,8 @@ static inline bool gemm_launch_sk(const GemmArgs &g, cudaStream_t s, cudaError_t
     if (tiles < slots) return false;
     const long waves = (tiles + slots - 1) / slots;
     if ((double)tiles / (double)(waves * slots) >= 0.97) return false;
-    static GmSkWS cache[8];
-    int dev = 0;
-    cudaGetDevice(&dev);
-    GmSkWS *w = nullptr;
-    for (GmSkWS &c : cache)
-        if (c.ws && c.dev == dev && c.stream == s) w = &c;
-    if (!w) {
-        for (GmSkWS &c : cache)
-            if (!c.ws) {
-                w = &c;
-                break;
-            }
-        if (!w) return false;
-        const size_t nacc = (size_t)GmGeo<CFG>::FI * GmGeo<CFG>::FJ * 2 * GmGeo<CFG>::THREADS;
-        if (cudaMalloc(&w->ws, sizeof(double) * nacc * slots) != cudaSuccess) {
-            w->ws = nullptr;
-            return false;
-        }
-        if (cudaMalloc(&w->flags, sizeof(unsigned) * slots) != cudaSuccess ||
-            cudaMemset(w->flags, 0, sizeof(unsigned) * slots) != cudaSuccess) {
-            cudaFree(w->ws);
-            w->ws = nullptr;
-            return false;
-        }
-        w->dev = dev;
-        w->stream = s;
-        w->grid = slots;
-    }
+    GmSkWS *w = gm_sk_ws(s, slots);
+    if (!w) return false;
     unsigned epoch = ++w->epoch;
     if (epoch == 0) epoch = ++w->epoch;  // 0 is the flags' initial value
     const int nkt = (g.K + GM_BK - 1) / GM_BK;

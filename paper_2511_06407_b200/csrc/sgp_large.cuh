@@ -34,6 +34,9 @@ struct LgPtrs {
     GemmArgs *bjDesc;            // [round][col A | row A | col V even | col V odd][2 * pairs]
     GemmArgs *hdesc;             // the likelihood-Hessian blocks' batched GEMM descriptors (4)
     double *hpart;               // second K half of the off-diagonal likelihood block (J = 2)
+    int4 *htiles;                // grouped stream-K tile list of the likelihood blocks (built once)
+    long *hprefix;
+    int hntiles;
     // host handles owned by this workspace (one per model, like the buffers above): the
     // high-priority stream of the block-Jacobi A chain and the events ordering it against
     // the caller's stream (in, solved, chain, V update of even / odd rounds)
@@ -1140,12 +1143,14 @@ static int lg_state(LgCtx &c, int qv, int what) {
             const int fields[3] = {F_D2_00, F_D2_01, F_D2_11};
             // the J(J+1)/2 likelihood blocks in one batched launch (each 1040 x 1040 block alone
             // fills about half a wave of the GPU at C4)
-            // diagonal blocks first (full K), then the off-diagonal block as two K halves (the
-            // second into hpart, added by k_lg_addt_block): at C4 595 64 x 64 tiles were 2.01 waves
-            // of 296 CTA slots; 884 tiles with half-length off-diagonal ones fill ~3 waves
+            // preferred: the J(J+1)/2 blocks as ONE grouped stream-K launch over 128 x 64 tiles
+            // (tile list built once per model); else the batched 64 x 64 launch below with the
+            // off-diagonal block split over K (595 tiles = 2.01 waves -> 884 tiles ~3 waves)
             GemmArgs hd[4];
             int nbk = 0, maxM = 0, maxN = 0;
-            const int kh = c.L.hpart ? ((mp.N / 2) & ~(GM_BK - 1)) : 0;
+            const char *skg_env = getenv("SGP_GEMM_STREAMK");
+            const bool grouped = c.L.hntiles > 0 && !(skg_env && skg_env[0] == '0');
+            const int kh = (c.L.hpart && !grouped) ? ((mp.N / 2) & ~(GM_BK - 1)) : 0;
             auto push = [&](int j1, int j2, int k0, int k1, double *C, int ldc) {
                 GemmArgs &g = hd[nbk++];
                 g = GemmArgs{};
@@ -1167,15 +1172,24 @@ static int lg_state(LgCtx &c, int qv, int what) {
                 maxM = std::max(maxM, g.M);
                 maxN = std::max(maxN, g.N);
             };
-            for (int j = 0; j < mp.J; ++j) push(j, j, 0, mp.N, c.L.H + (size_t)mp.fstart[j] * d + mp.fstart[j], d);
-            const bool split = mp.J == 2 && kh > 0;
-            if (mp.J == 2) {
-                push(0, 1, 0, split ? kh : mp.N, c.L.H + (size_t)mp.fstart[0] * d + mp.fstart[1], d);
-                if (split) push(0, 1, kh, mp.N, c.L.hpart, mp.D[1]);
+            bool split = false;
+            if (grouped) {  // descriptor order = the tile list's (j1 <= j2)
+                for (int j1 = 0; j1 < mp.J; ++j1)
+                    for (int j2 = j1; j2 < mp.J; ++j2)
+                        push(j1, j2, 0, mp.N, c.L.H + (size_t)mp.fstart[j1] * d + mp.fstart[j2], d);
+            } else {
+                for (int j = 0; j < mp.J; ++j)
+                    push(j, j, 0, mp.N, c.L.H + (size_t)mp.fstart[j] * d + mp.fstart[j], d);
+                split = mp.J == 2 && kh > 0;
+                if (mp.J == 2) {
+                    push(0, 1, 0, split ? kh : mp.N, c.L.H + (size_t)mp.fstart[0] * d + mp.fstart[1], d);
+                    if (split) push(0, 1, kh, mp.N, c.L.hpart, mp.D[1]);
+                }
             }
             // all blocks share TA/TB; the alignment flags agree (same Phi buffer, same ld)
             cudaMemcpyAsync(c.L.hdesc, hd, sizeof(GemmArgs) * nbk, cudaMemcpyHostToDevice, c.s);
-            gemm_launch_batched<1, 0>(c.L.hdesc, nbk, maxM, maxN, c.s);
+            if (!(grouped && gemm_launch_skg<1, 0>(c.L.hdesc, c.L.htiles, c.L.hprefix, c.L.hntiles, c.s)))
+                gemm_launch_batched<1, 0>(c.L.hdesc, nbk, maxM, maxN, c.s);
             for (int j1 = 0; j1 < mp.J; ++j1)
                 for (int j2 = j1; j2 < mp.J; ++j2) {
                     if (j1 == j2)
@@ -1924,7 +1938,25 @@ static int lg_alloc(const ModelDev &M, LgPtrs &L, void **owner) {
     const size_t ndesc = (size_t)(nbk - 1) * 4 * bnp;
     const size_t obD = take((ndesc * sizeof(GemmArgs) + sizeof(double) - 1) / sizeof(double) + 2);
     const size_t ohD = take((4 * sizeof(GemmArgs) + sizeof(double) - 1) / sizeof(double) + 2);
-    const size_t ohp = take(M.mp.J == 2 ? (size_t)M.mp.D[0] * M.mp.D[1] : 0);
+    // grouped stream-K tile list of the likelihood Hessian blocks (j1 <= j2; diagonal blocks upper)
+    std::vector<int4> htl;
+    std::vector<long> hpf;
+    {
+        GemmArgs shp[3];
+        int nb = 0;
+        for (int j1 = 0; j1 < M.mp.J; ++j1)
+            for (int j2 = j1; j2 < M.mp.J; ++j2) {
+                shp[nb] = GemmArgs{};
+                shp[nb].M = M.mp.D[j1];
+                shp[nb].N = M.mp.D[j2];
+                shp[nb].K = M.mp.N;
+                shp[nb].upper_only = j1 == j2;
+                ++nb;
+            }
+        if (M.mp.lik != SGP_LIK_QUADRATIC && M.mp.N > 0) gemm_group_tiles(shp, nb, htl, hpf);
+    }
+    const size_t oht = take(2 * htl.size() + 2), ohp = take(hpf.size() + 1);
+    const size_t ohp_part = take(M.mp.J == 2 ? (size_t)M.mp.D[0] * M.mp.D[1] : 0);
     double *base = nullptr;
     if (cudaMalloc(&base, off * sizeof(double)) != cudaSuccess) return SGP_ENOMEM;
     cudaMemset(base, 0, off * sizeof(double));
@@ -1957,7 +1989,13 @@ static int lg_alloc(const ModelDev &M, LgPtrs &L, void **owner) {
     L.bjCnt = reinterpret_cast<int *>(base + obC);
     L.bjDesc = reinterpret_cast<GemmArgs *>(base + ((obD + 1) & ~size_t(1)));  // 16-byte aligned
     L.hdesc = reinterpret_cast<GemmArgs *>(base + ((ohD + 1) & ~size_t(1)));
-    L.hpart = M.mp.J == 2 ? base + ohp : nullptr;
+    L.hpart = M.mp.J == 2 ? base + ohp_part : nullptr;
+    L.htiles = reinterpret_cast<int4 *>(base + ((oht + 1) & ~size_t(1)));
+    L.hprefix = reinterpret_cast<long *>(base + ohp);
+    L.hntiles = (int)htl.size();
+    if (!htl.empty() && (cudaMemcpy(L.htiles, htl.data(), sizeof(int4) * htl.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
+                         cudaMemcpy(L.hprefix, hpf.data(), sizeof(long) * hpf.size(), cudaMemcpyHostToDevice) != cudaSuccess))
+        L.hntiles = 0;
     {
         L.bj_hs = nullptr;
         for (cudaEvent_t &e : L.bj_ev) e = nullptr;
