@@ -21,6 +21,7 @@
 #include "sgp_dc.cuh"
 
 #define LG_NT 256
+#define LG_NCORR 4  // warm calls per leapfrog with a stored refinement correction
 
 struct LgPtrs {
     ModelDev M;
@@ -34,7 +35,7 @@ struct LgPtrs {
     GemmArgs *bjDesc;            // [round][col A | row A | col V even | col V odd][2 * pairs]
     GemmArgs *hdesc;             // the likelihood-Hessian blocks' batched GEMM descriptors (4)
     double *hpart;               // second K half of the off-diagonal likelihood block (J = 2)
-    double *Pprev;               // the previous frame's basis (refinement warm-start extrapolation)
+    double *Dcorr[LG_NCORR];     // per warm-call index: the previous leapfrog's refinement correction
     int4 *htiles;                // grouped stream-K tile list of the likelihood blocks (built once)
     long *hprefix;
     int hntiles;
@@ -1029,9 +1030,12 @@ struct LgCtx {
     int si[16];
     int status;
     int since[2];
-    // warm-start extrapolation of the refinement (first warm call of a leapfrog):
-    // have_prev = Pprev holds the previous frame's basis, in the current basis's column order
-    bool have_prev, extrap_next, basis_reset;
+    // refinement warm start by correction transfer: call i of a leapfrog's position fixed point
+    // starts from its natural basis S plus the correction R - S that call i made in the previous
+    // leapfrog (Dcorr[i], valid while the trajectory and the column order continue)
+    bool corr_valid[LG_NCORR];
+    int warm_idx;      // index of the warm call being made (-1: none / no transfer)
+    bool basis_reset;
 };
 
 static void lg_op(LgCtx &c, int op, int slot = 0, int a0 = 0, int a1 = 0, int i0 = 0, double eps = 0.0) {
@@ -1704,10 +1708,10 @@ static void lg_gemm_ab(LgCtx &c, int M, int N, int K, const double *A, int lda, 
 
 static int lg_eig_warm_jacobi(LgCtx &c, int src, int dst, int *sweeps);
 
-// out = a + (a - b): linear extrapolation of the eigenvector basis from the last two frames
-__global__ void k_lg_extrap(double *out, const double *a, const double *b, size_t n) {
+// out = a + b (warm start: natural basis + transferred correction); out = a - b (correction)
+__global__ void k_lg_axpb(double *out, const double *a, const double *b, double sb, size_t n) {
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
-        out[i] = a[i] + (a[i] - b[i]);
+        out[i] = a[i] + sb * b[i];
 }
 
 static int lg_eig_refine(LgCtx &c, int src, int dst, int *sweeps) {
@@ -1720,15 +1724,14 @@ static int lg_eig_refine(LgCtx &c, int src, int dst, int *sweeps) {
     lg_symmetrize(c.L.H, d, c.s);
     double *psi = c.L.P[dst], *Y = c.L.X, *Sm = c.L.W, *G = c.L.bjA, *E = c.L.bjT, *Pn = c.L.bjV[0];
     double *lam = c.L.vec + (size_t)V_TMP * d;  // scratch d-vector (free during the eigensolver)
-    if (c.extrap_next && c.L.Pprev) {
-        // first warm call of a leapfrog: start from the basis extrapolated along the trajectory
-        // (the previous leapfrog moved the eigenvectors by ~1e-5; the prediction error is
-        // second order, so the refinement needs one iteration fewer)
-        k_lg_extrap<<<lg_blocks(dd), 256, 0, c.s>>>(psi, c.L.P[src], c.L.Pprev, dd);
+    const int wi = c.warm_idx;
+    if (wi >= 0 && wi < LG_NCORR && c.corr_valid[wi]) {
+        // start from the natural basis plus the correction this call made in the previous leapfrog
+        // (the fixed-point iterates move smoothly along the trajectory: one iteration fewer)
+        k_lg_axpb<<<lg_blocks(dd), 256, 0, c.s>>>(psi, c.L.P[src], c.L.Dcorr[wi], 1.0, dd);
     } else {
         k_lg_copy<<<lg_blocks(dd), 256, 0, c.s>>>(psi, c.L.P[src], dd);
     }
-    c.extrap_next = false;
     const int nb = OA_NB;  // two partials per CTA in bjPart
     double prev_off = INFINITY;
     for (int it = 0;; ++it) {
@@ -1789,7 +1792,7 @@ static int lg_eig_refine(LgCtx &c, int src, int dst, int *sweeps) {
     const char *fb = getenv("SGP_REFINE_FALLBACK");
     if (!(fb && strcmp(fb, "jacobi") == 0) && c.L.dc && d <= DC_NMAX) {
         if (getenv("SGP_DEBUG_REFINE")) fprintf(stderr, "refine -> divide-and-conquer fallback\n");
-        c.basis_reset = true;  // new column order: no extrapolation across this frame
+        c.basis_reset = true;  // new column order: no correction transfer across this call
         if (dc_eigh(*c.L.dc, c.L.H, d, d, lam, c.L.P[dst], d, c.s)) return SGP_STATUS_JACOBI;
         k_lg_set_diag<<<lg_blocks(d), 256, 0, c.s>>>(c.L.H, lam, d);
         *sweeps = std::min(c.cfg.sweep_cap, 8) + 1;
@@ -1870,19 +1873,25 @@ static int lg_leapfrog(LgCtx &c, int &f, int *fp_p, int *fp_q, double *sweep_sum
                     cudaMemcpyDeviceToDevice, c.s);
     int prev = f, cur = f;
     conv = false;
-    static const bool extrap_on = !(getenv("SGP_REFINE_EXTRAP") && getenv("SGP_REFINE_EXTRAP")[0] == '0');
-    const bool extrap = extrap_on && c.have_prev && c.cfg.metric == SGP_METRIC_DYNAMIC &&
-                        c.cfg.warm_order == SGP_ORDER_REFINE && c.L.Pprev;
-    c.basis_reset = false;
+    static const bool transfer_on = !(getenv("SGP_REFINE_TRANSFER") && getenv("SGP_REFINE_TRANSFER")[0] == '0');
+    const bool transfer = transfer_on && c.cfg.metric == SGP_METRIC_DYNAMIC && c.cfg.warm_order == SGP_ORDER_REFINE;
     for (int it = 0; it < c.cfg.fp_max_iters; ++it) {
         if ((st = lg_state(c, V_QC, SGP_EVAL_HESSIAN))) return st;
         const int nxt = 1 - prev;
         int sw = 0;
-        c.extrap_next = extrap && it == 0;
+        c.warm_idx = transfer ? it : -1;
+        c.basis_reset = false;
         st = c.cfg.metric == SGP_METRIC_STATIC ? lg_eig_cold(c, nxt, &sw) : lg_eig_warm(c, prev, nxt, &sw);
-        c.extrap_next = false;
-        if (it == 0 && c.L.Pprev && c.cfg.warm_order == SGP_ORDER_REFINE)  // this leapfrog's frame -> Pprev
-            k_lg_copy<<<lg_blocks((size_t)d * d), 256, 0, c.s>>>(c.L.Pprev, c.L.P[f], (size_t)d * d);
+        c.warm_idx = -1;
+        if (transfer && it < LG_NCORR) {
+            if (c.basis_reset) {  // a hand-over changed the column order: drop every stored correction
+                for (bool &v : c.corr_valid) v = false;
+            } else {  // this call's correction R - S for the next leapfrog
+                k_lg_axpb<<<lg_blocks((size_t)d * d), 256, 0, c.s>>>(c.L.Dcorr[it], c.L.P[nxt], c.L.P[prev], -1.0,
+                                                                    (size_t)d * d);
+                c.corr_valid[it] = true;
+            }
+        }
         if (sweep_log && it < 32) sweep_log[it] = sw;
         if (st) return st;
         *sweep_sum += sw;
@@ -1902,7 +1911,6 @@ static int lg_leapfrog(LgCtx &c, int &f, int *fp_p, int *fp_q, double *sweep_sum
     }
     if (!conv) return SGP_STATUS_STALL_Q;
     f = cur;
-    c.have_prev = !c.basis_reset;
     lg_contraction(c, f, V_PH);
     if ((st = lg_state(c, V_QC, SGP_EVAL_GRADIENT | SGP_EVAL_REUSE))) return st;
     if ((st = lg_trace(c, V_QC))) return st;
@@ -1984,7 +1992,7 @@ static int lg_alloc(const ModelDev &M, LgPtrs &L, void **owner) {
             }
         if (M.mp.lik != SGP_LIK_QUADRATIC && M.mp.N > 0) gemm_group_tiles(shp, nb, htl, hpf);
     }
-    const size_t oht = take(2 * htl.size() + 2), ohp = take(hpf.size() + 1), opp = take(dd);
+    const size_t oht = take(2 * htl.size() + 2), ohp = take(hpf.size() + 1), odc = take(LG_NCORR * dd);
     const size_t ohp_part = take(M.mp.J == 2 ? (size_t)M.mp.D[0] * M.mp.D[1] : 0);
     double *base = nullptr;
     if (cudaMalloc(&base, off * sizeof(double)) != cudaSuccess) return SGP_ENOMEM;
@@ -2021,7 +2029,7 @@ static int lg_alloc(const ModelDev &M, LgPtrs &L, void **owner) {
     L.hpart = M.mp.J == 2 ? base + ohp_part : nullptr;
     L.htiles = reinterpret_cast<int4 *>(base + ((oht + 1) & ~size_t(1)));
     L.hprefix = reinterpret_cast<long *>(base + ohp);
-    L.Pprev = base + opp;
+    for (int k = 0; k < LG_NCORR; ++k) L.Dcorr[k] = base + odc + k * dd;
     L.hntiles = (int)htl.size();
     if (!htl.empty() && (cudaMemcpy(L.htiles, htl.data(), sizeof(int4) * htl.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
                          cudaMemcpy(L.hprefix, hpf.data(), sizeof(long) * hpf.size(), cudaMemcpyHostToDevice) != cudaSuccess))
@@ -2085,7 +2093,9 @@ static void lg_ctx(LgCtx &c, const LgPtrs &L, const sgp_chain_config &cfg, doubl
     c.tau = tau;
     c.d = L.M.mp.d;
     c.since[0] = c.since[1] = 0;
-    c.have_prev = c.extrap_next = c.basis_reset = false;
+    for (bool &v : c.corr_valid) v = false;
+    c.warm_idx = -1;
+    c.basis_reset = false;
     memset(c.sc, 0, sizeof(c.sc));
     memset(c.si, 0, sizeof(c.si));
     c.status = 0;
@@ -2203,7 +2213,7 @@ static int lg_run_moves(const LgPtrs &L, const sgp_chain_config *cfg, const sgp_
             double sweep_sum = 0.0;
             int sweep_cnt = 0;
             int fr = f, ls = 0;
-            c.have_prev = false;  // a new momentum: no extrapolation from the previous trajectory
+            for (bool &v : c.corr_valid) v = false;  // a new momentum: nothing to transfer
             for (int l = 0; l < cfg->leapfrogs && !ls; ++l)
                 ls = euclid ? lg_euclid_leapfrog(c) : lg_leapfrog(c, fr, nullptr, nullptr, &sweep_sum, &sweep_cnt,
                                                                    nullptr);
