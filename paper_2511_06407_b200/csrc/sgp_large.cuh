@@ -35,7 +35,7 @@ struct LgPtrs {
     GemmArgs *bjDesc;            // [round][col A | row A | col V even | col V odd][2 * pairs]
     GemmArgs *hdesc;             // the likelihood-Hessian blocks' batched GEMM descriptors (4)
     double *hpart;               // second K half of the off-diagonal likelihood block (J = 2)
-    double *Dcorr[LG_NCORR];     // per warm-call index: the previous leapfrog's refinement correction
+    double *Dcorr[LG_NCORR][2];  // per warm-call index: the last two leapfrogs' refinement corrections
     int4 *htiles;                // grouped stream-K tile list of the likelihood blocks (built once)
     long *hprefix;
     int hntiles;
@@ -1033,7 +1033,10 @@ struct LgCtx {
     // refinement warm start by correction transfer: call i of a leapfrog's position fixed point
     // starts from its natural basis S plus the correction R - S that call i made in the previous
     // leapfrog (Dcorr[i], valid while the trajectory and the column order continue)
-    bool corr_valid[LG_NCORR];
+    int corr_n[LG_NCORR];  // stored corrections of call i (0, 1 or 2: D(k-1) and D(k-2))
+    int corr_cur[LG_NCORR];  // which of the two buffers holds D(k-1)
+    long corr_lf[LG_NCORR][2];  // leapfrog index each stored correction was made in
+    long lf_count;              // leapfrogs made by this context
     int warm_idx;      // index of the warm call being made (-1: none / no transfer)
     bool basis_reset;
 };
@@ -1708,10 +1711,12 @@ static void lg_gemm_ab(LgCtx &c, int M, int N, int K, const double *A, int lda, 
 
 static int lg_eig_warm_jacobi(LgCtx &c, int src, int dst, int *sweeps);
 
-// out = a + b (warm start: natural basis + transferred correction); out = a - b (correction)
-__global__ void k_lg_axpb(double *out, const double *a, const double *b, double sb, size_t n) {
+// out = a + sb b (warm start: natural basis + transferred correction; correction = a - b), or with
+// a second correction c: out = a + (2 b - c) (the correction extrapolated linearly over leapfrogs)
+__global__ void k_lg_axpb(double *out, const double *a, const double *b, double sb, size_t n,
+                          const double *c = nullptr) {
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
-        out[i] = a[i] + sb * b[i];
+        out[i] = c ? a[i] + (2.0 * b[i] - c[i]) : a[i] + sb * b[i];
 }
 
 static int lg_eig_refine(LgCtx &c, int src, int dst, int *sweeps) {
@@ -1725,10 +1730,15 @@ static int lg_eig_refine(LgCtx &c, int src, int dst, int *sweeps) {
     double *psi = c.L.P[dst], *Y = c.L.X, *Sm = c.L.W, *G = c.L.bjA, *E = c.L.bjT, *Pn = c.L.bjV[0];
     double *lam = c.L.vec + (size_t)V_TMP * d;  // scratch d-vector (free during the eigensolver)
     const int wi = c.warm_idx;
-    if (wi >= 0 && wi < LG_NCORR && c.corr_valid[wi]) {
-        // start from the natural basis plus the correction this call made in the previous leapfrog
-        // (the fixed-point iterates move smoothly along the trajectory: one iteration fewer)
-        k_lg_axpb<<<lg_blocks(dd), 256, 0, c.s>>>(psi, c.L.P[src], c.L.Dcorr[wi], 1.0, dd);
+    if (wi >= 0 && wi < LG_NCORR && c.corr_n[wi] > 0 && c.corr_lf[wi][c.corr_cur[wi]] == c.lf_count - 1) {
+        // start from the natural basis plus the correction this call made in the previous leapfrog,
+        // extrapolated linearly when two are stored (the fixed-point iterates move smoothly along
+        // the trajectory)
+        static const bool second = !(getenv("SGP_REFINE_TRANSFER") && getenv("SGP_REFINE_TRANSFER")[0] == '1');
+        const int cur = c.corr_cur[wi];
+        const bool two = second && c.corr_n[wi] > 1 && c.corr_lf[wi][1 - cur] == c.lf_count - 2;
+        k_lg_axpb<<<lg_blocks(dd), 256, 0, c.s>>>(psi, c.L.P[src], c.L.Dcorr[wi][cur], 1.0, dd,
+                                                   two ? c.L.Dcorr[wi][1 - cur] : nullptr);
     } else {
         k_lg_copy<<<lg_blocks(dd), 256, 0, c.s>>>(psi, c.L.P[src], dd);
     }
@@ -1885,11 +1895,14 @@ static int lg_leapfrog(LgCtx &c, int &f, int *fp_p, int *fp_q, double *sweep_sum
         c.warm_idx = -1;
         if (transfer && it < LG_NCORR) {
             if (c.basis_reset) {  // a hand-over changed the column order: drop every stored correction
-                for (bool &v : c.corr_valid) v = false;
-            } else {  // this call's correction R - S for the next leapfrog
-                k_lg_axpb<<<lg_blocks((size_t)d * d), 256, 0, c.s>>>(c.L.Dcorr[it], c.L.P[nxt], c.L.P[prev], -1.0,
-                                                                    (size_t)d * d);
-                c.corr_valid[it] = true;
+                for (int k = 0; k < LG_NCORR; ++k) c.corr_n[k] = 0;
+            } else {  // this call's correction R - S for the next leapfrog (the older one is kept)
+                const int slot = c.corr_n[it] > 0 ? 1 - c.corr_cur[it] : c.corr_cur[it];
+                k_lg_axpb<<<lg_blocks((size_t)d * d), 256, 0, c.s>>>(c.L.Dcorr[it][slot], c.L.P[nxt], c.L.P[prev],
+                                                                    -1.0, (size_t)d * d);
+                c.corr_cur[it] = slot;
+                c.corr_lf[it][slot] = c.lf_count;
+                c.corr_n[it] = std::min(2, c.corr_n[it] + 1);
             }
         }
         if (sweep_log && it < 32) sweep_log[it] = sw;
@@ -1911,6 +1924,7 @@ static int lg_leapfrog(LgCtx &c, int &f, int *fp_p, int *fp_q, double *sweep_sum
     }
     if (!conv) return SGP_STATUS_STALL_Q;
     f = cur;
+    ++c.lf_count;
     lg_contraction(c, f, V_PH);
     if ((st = lg_state(c, V_QC, SGP_EVAL_GRADIENT | SGP_EVAL_REUSE))) return st;
     if ((st = lg_trace(c, V_QC))) return st;
@@ -1992,7 +2006,7 @@ static int lg_alloc(const ModelDev &M, LgPtrs &L, void **owner) {
             }
         if (M.mp.lik != SGP_LIK_QUADRATIC && M.mp.N > 0) gemm_group_tiles(shp, nb, htl, hpf);
     }
-    const size_t oht = take(2 * htl.size() + 2), ohp = take(hpf.size() + 1), odc = take(LG_NCORR * dd);
+    const size_t oht = take(2 * htl.size() + 2), ohp = take(hpf.size() + 1), odc = take(2 * LG_NCORR * dd);
     const size_t ohp_part = take(M.mp.J == 2 ? (size_t)M.mp.D[0] * M.mp.D[1] : 0);
     double *base = nullptr;
     if (cudaMalloc(&base, off * sizeof(double)) != cudaSuccess) return SGP_ENOMEM;
@@ -2029,7 +2043,8 @@ static int lg_alloc(const ModelDev &M, LgPtrs &L, void **owner) {
     L.hpart = M.mp.J == 2 ? base + ohp_part : nullptr;
     L.htiles = reinterpret_cast<int4 *>(base + ((oht + 1) & ~size_t(1)));
     L.hprefix = reinterpret_cast<long *>(base + ohp);
-    for (int k = 0; k < LG_NCORR; ++k) L.Dcorr[k] = base + odc + k * dd;
+    for (int k = 0; k < LG_NCORR; ++k)
+        for (int h = 0; h < 2; ++h) L.Dcorr[k][h] = base + odc + (2 * k + h) * dd;
     L.hntiles = (int)htl.size();
     if (!htl.empty() && (cudaMemcpy(L.htiles, htl.data(), sizeof(int4) * htl.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
                          cudaMemcpy(L.hprefix, hpf.data(), sizeof(long) * hpf.size(), cudaMemcpyHostToDevice) != cudaSuccess))
@@ -2093,7 +2108,8 @@ static void lg_ctx(LgCtx &c, const LgPtrs &L, const sgp_chain_config &cfg, doubl
     c.tau = tau;
     c.d = L.M.mp.d;
     c.since[0] = c.since[1] = 0;
-    for (bool &v : c.corr_valid) v = false;
+    for (int k = 0; k < LG_NCORR; ++k) c.corr_n[k] = c.corr_cur[k] = 0;
+    c.lf_count = 0;
     c.warm_idx = -1;
     c.basis_reset = false;
     memset(c.sc, 0, sizeof(c.sc));
@@ -2213,7 +2229,7 @@ static int lg_run_moves(const LgPtrs &L, const sgp_chain_config *cfg, const sgp_
             double sweep_sum = 0.0;
             int sweep_cnt = 0;
             int fr = f, ls = 0;
-            for (bool &v : c.corr_valid) v = false;  // a new momentum: nothing to transfer
+            for (int k = 0; k < LG_NCORR; ++k) c.corr_n[k] = 0;  // a new momentum: nothing to transfer
             for (int l = 0; l < cfg->leapfrogs && !ls; ++l)
                 ls = euclid ? lg_euclid_leapfrog(c) : lg_leapfrog(c, fr, nullptr, nullptr, &sweep_sum, &sweep_cnt,
                                                                    nullptr);
