@@ -35,7 +35,7 @@ struct LgPtrs {
     GemmArgs *bjDesc;            // [round][col A | row A | col V even | col V odd][2 * pairs]
     GemmArgs *hdesc;             // the likelihood-Hessian blocks' batched GEMM descriptors (4)
     double *hpart;               // second K half of the off-diagonal likelihood block (J = 2)
-    double *Dcorr[LG_NCORR][2];  // per warm-call index: the last two leapfrogs' refinement corrections
+    double *Dcorr[LG_NCORR][3];  // per warm-call index: the last three leapfrogs' refinement corrections
     int4 *htiles;                // grouped stream-K tile list of the likelihood blocks (built once)
     long *hprefix;
     int hntiles;
@@ -1033,9 +1033,9 @@ struct LgCtx {
     // refinement warm start by correction transfer: call i of a leapfrog's position fixed point
     // starts from its natural basis S plus the correction R - S that call i made in the previous
     // leapfrog (Dcorr[i], valid while the trajectory and the column order continue)
-    int corr_n[LG_NCORR];  // stored corrections of call i (0, 1 or 2: D(k-1) and D(k-2))
-    int corr_cur[LG_NCORR];  // which of the two buffers holds D(k-1)
-    long corr_lf[LG_NCORR][2];  // leapfrog index each stored correction was made in
+    int corr_n[LG_NCORR];       // stored corrections of call i (up to 3: D(k-1), D(k-2), D(k-3))
+    int corr_cur[LG_NCORR];     // ring slot holding D(k-1); D(k-j) at (cur - j + 1) mod 3
+    long corr_lf[LG_NCORR][3];  // leapfrog index each stored correction was made in
     long lf_count;              // leapfrogs made by this context
     int warm_idx;      // index of the warm call being made (-1: none / no transfer)
     bool basis_reset;
@@ -1711,12 +1711,13 @@ static void lg_gemm_ab(LgCtx &c, int M, int N, int K, const double *A, int lda, 
 
 static int lg_eig_warm_jacobi(LgCtx &c, int src, int dst, int *sweeps);
 
-// out = a + sb b (warm start: natural basis + transferred correction; correction = a - b), or with
-// a second correction c: out = a + (2 b - c) (the correction extrapolated linearly over leapfrogs)
+// out = a + sb b (warm start: natural basis + transferred correction; correction = a - b); with
+// older corrections c (and e) the correction is extrapolated over leapfrogs: a + (2b - c) linearly,
+// a + (3b - 3c + e) quadratically
 __global__ void k_lg_axpb(double *out, const double *a, const double *b, double sb, size_t n,
-                          const double *c = nullptr) {
+                          const double *c = nullptr, const double *e = nullptr) {
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
-        out[i] = c ? a[i] + (2.0 * b[i] - c[i]) : a[i] + sb * b[i];
+        out[i] = e ? a[i] + (3.0 * (b[i] - c[i]) + e[i]) : (c ? a[i] + (2.0 * b[i] - c[i]) : a[i] + sb * b[i]);
 }
 
 static int lg_eig_refine(LgCtx &c, int src, int dst, int *sweeps) {
@@ -1734,11 +1735,17 @@ static int lg_eig_refine(LgCtx &c, int src, int dst, int *sweeps) {
         // start from the natural basis plus the correction this call made in the previous leapfrog,
         // extrapolated linearly when two are stored (the fixed-point iterates move smoothly along
         // the trajectory)
-        static const bool second = !(getenv("SGP_REFINE_TRANSFER") && getenv("SGP_REFINE_TRANSFER")[0] == '1');
-        const int cur = c.corr_cur[wi];
-        const bool two = second && c.corr_n[wi] > 1 && c.corr_lf[wi][1 - cur] == c.lf_count - 2;
+        // extrapolation order per call (measured at C4): the first call moves a whole step and
+        // takes the quadratic fit, the second the linear one; later calls' corrections are tiny
+        // and noisy, extrapolating them only amplifies the noise
+        static const int max_order = getenv("SGP_REFINE_TRANSFER") ? atoi(getenv("SGP_REFINE_TRANSFER")) : 3;
+        const int want = std::min(max_order, wi == 0 ? 3 : (wi == 1 ? 2 : 1));
+        const int cur = c.corr_cur[wi], p1 = (cur + 2) % 3, p2 = (cur + 1) % 3;
+        const bool two = want >= 2 && c.corr_n[wi] >= 2 && c.corr_lf[wi][p1] == c.lf_count - 2;
+        const bool three = two && want >= 3 && c.corr_n[wi] >= 3 && c.corr_lf[wi][p2] == c.lf_count - 3;
         k_lg_axpb<<<lg_blocks(dd), 256, 0, c.s>>>(psi, c.L.P[src], c.L.Dcorr[wi][cur], 1.0, dd,
-                                                   two ? c.L.Dcorr[wi][1 - cur] : nullptr);
+                                                   two ? c.L.Dcorr[wi][p1] : nullptr,
+                                                   three ? c.L.Dcorr[wi][p2] : nullptr);
     } else {
         k_lg_copy<<<lg_blocks(dd), 256, 0, c.s>>>(psi, c.L.P[src], dd);
     }
@@ -1897,12 +1904,12 @@ static int lg_leapfrog(LgCtx &c, int &f, int *fp_p, int *fp_q, double *sweep_sum
             if (c.basis_reset) {  // a hand-over changed the column order: drop every stored correction
                 for (int k = 0; k < LG_NCORR; ++k) c.corr_n[k] = 0;
             } else {  // this call's correction R - S for the next leapfrog (the older one is kept)
-                const int slot = c.corr_n[it] > 0 ? 1 - c.corr_cur[it] : c.corr_cur[it];
+                const int slot = c.corr_n[it] > 0 ? (c.corr_cur[it] + 1) % 3 : c.corr_cur[it];
                 k_lg_axpb<<<lg_blocks((size_t)d * d), 256, 0, c.s>>>(c.L.Dcorr[it][slot], c.L.P[nxt], c.L.P[prev],
                                                                     -1.0, (size_t)d * d);
                 c.corr_cur[it] = slot;
                 c.corr_lf[it][slot] = c.lf_count;
-                c.corr_n[it] = std::min(2, c.corr_n[it] + 1);
+                c.corr_n[it] = std::min(3, c.corr_n[it] + 1);
             }
         }
         if (sweep_log && it < 32) sweep_log[it] = sw;
@@ -2006,7 +2013,7 @@ static int lg_alloc(const ModelDev &M, LgPtrs &L, void **owner) {
             }
         if (M.mp.lik != SGP_LIK_QUADRATIC && M.mp.N > 0) gemm_group_tiles(shp, nb, htl, hpf);
     }
-    const size_t oht = take(2 * htl.size() + 2), ohp = take(hpf.size() + 1), odc = take(2 * LG_NCORR * dd);
+    const size_t oht = take(2 * htl.size() + 2), ohp = take(hpf.size() + 1), odc = take(3 * LG_NCORR * dd);
     const size_t ohp_part = take(M.mp.J == 2 ? (size_t)M.mp.D[0] * M.mp.D[1] : 0);
     double *base = nullptr;
     if (cudaMalloc(&base, off * sizeof(double)) != cudaSuccess) return SGP_ENOMEM;
@@ -2044,7 +2051,7 @@ static int lg_alloc(const ModelDev &M, LgPtrs &L, void **owner) {
     L.htiles = reinterpret_cast<int4 *>(base + ((oht + 1) & ~size_t(1)));
     L.hprefix = reinterpret_cast<long *>(base + ohp);
     for (int k = 0; k < LG_NCORR; ++k)
-        for (int h = 0; h < 2; ++h) L.Dcorr[k][h] = base + odc + (2 * k + h) * dd;
+        for (int h = 0; h < 3; ++h) L.Dcorr[k][h] = base + odc + (3 * k + h) * dd;
     L.hntiles = (int)htl.size();
     if (!htl.empty() && (cudaMemcpy(L.htiles, htl.data(), sizeof(int4) * htl.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
                          cudaMemcpy(L.hprefix, hpf.data(), sizeof(long) * hpf.size(), cudaMemcpyHostToDevice) != cudaSuccess))
