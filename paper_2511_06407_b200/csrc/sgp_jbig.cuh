@@ -258,16 +258,34 @@ __device__ __forceinline__ void jb_lookahead(const JbArgs &a, const JbShared &sh
         double e[JB_W];
 #pragma unroll
         for (int j = 0; j < JB_W; ++j) e[j] = (valid && j < n) ? __ldcg(seg + j) : 0.0;
+        JB_T0(tlb);
         asm volatile("bar.sync 4, 64;" ::: "memory");  // the chain wrote the window's ring
+        if (lane == 0) JB_ACC(9, tlb);
+        JB_T0(tlf);
         const double *rc = sh.rc[seq & 1], *rs = sh.rs[seq & 1];
         const int *rf = sh.rf[seq & 1];
+        // ring read 8 rotations ahead of the arithmetic, flags applied by selection (the same
+        // rounded operations as a per-rotation branch, without a shared-memory load on the
+        // serial path of every step)
 #pragma unroll
-        for (int j = 0; j < JB_W; ++j) {
-            if (j < n && rf[j]) {
-                const double c = rc[j], s = rs[j];
+        for (int j0 = 0; j0 < JB_W; j0 += 8) {
+            double cj[8], sj[8];
+            int fj[8];
+#pragma unroll
+            for (int t = 0; t < 8; ++t) {
+                cj[t] = rc[j0 + t];
+                sj[t] = rs[j0 + t];
+                fj[t] = rf[j0 + t];
+            }
+#pragma unroll
+            for (int t = 0; t < 8; ++t) {
+                const int j = j0 + t;
+                const bool on = j < n && fj[t] != 0;
                 const double akp = r, akq = e[j];
-                r = __dsub_rn(__dmul_rn(c, akp), __dmul_rn(s, akq));
-                e[j] = __dadd_rn(__dmul_rn(s, akp), __dmul_rn(c, akq));
+                const double nr = __dsub_rn(__dmul_rn(cj[t], akp), __dmul_rn(sj[t], akq));
+                const double ne = __dadd_rn(__dmul_rn(sj[t], akp), __dmul_rn(cj[t], akq));
+                r = on ? nr : r;
+                e[j] = on ? ne : e[j];
             }
         }
         if (valid) {
@@ -276,6 +294,7 @@ __device__ __forceinline__ void jb_lookahead(const JbArgs &a, const JbShared &sh
             for (int j = 0; j < JB_W; ++j)
                 if (j < n) __stcg(seg + j, e[j]);
         }
+        if (lane == 0) JB_ACC(10, tlf);
     }
     // no fence here: these stores are ordered before the io warps' fence and release of this
     // window by the CTA barrier that ends it (happens-before is transitive across the scopes)

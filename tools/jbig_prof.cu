@@ -45,8 +45,10 @@ int main(int argc, char **argv) {
         const double nwin = (double)p[8];
         printf("cap %d: sweeps %d, %.1f ms, windows %.0f\n", c, sw, ms, nwin);
         const char *names[] = {"chain window", "chain start barrier", "lookahead", "lookahead owner wait",
-                               "io publish", "io deferred load", "io prefetch", "end barrier (warp 0)"};
-        for (int i = 0; i < 8; ++i) printf("  %-24s %10.0f cycles/window\n", names[i], p[i] / nwin);
+                               "io publish", "io deferred load", "io prefetch", "end barrier (warp 0)",
+                               "windows", "lookahead wait for chain", "lookahead fold+stores"};
+        for (int i = 0; i < 11; ++i)
+            if (i != 8) printf("  %-24s %10.0f cycles/window\n", names[i], p[i] / nwin);
     }
     return 0;
 }
