@@ -905,7 +905,6 @@ static inline int dc_ws_alloc(DcWS &w, int n) {
         return -1;
     const int G = std::min(sms, DC_MAXG);  // one CTA per SM (co-resident: cooperative launch)
     if (n > DC_RPW * G * (DC_PT / 32)) return -1;  // rows per warp held in registers
-    const int npan = (n + DC_NB - 2) / DC_NB;
     const int nbt = std::max(1, (n - 1 + DC_BT - 1) / DC_BT);  // back-transform blocks
     size_t off = 0;
     auto take = [&](size_t cnt) {

@@ -143,7 +143,7 @@ __device__ __forceinline__ void tri_decode(int t, int nb, int &bi, int &bj) {
 template <int J>
 __device__ __noinline__ void hess_lik_tiled(EvalCtx &E, double tau, double *H, int d) {
     const ModelParams &mp = E.M.mp;
-    const int CH = E.CH, SP = mp.Dp + 2, nb = mp.Dp >> 2, ld = mp.ld;
+    const int CH = E.CH, SP = mp.Dp + 2, nb = mp.Dp >> 2;
     const int ntile = nb * (nb + 1) / 2;
     // sample replicas per tile: the R in 1..8 with the fewest rounds per sample
     int R = 1;
