@@ -269,7 +269,7 @@ extern "C" int sgp_model_features(const sgp_model *m, int j) {
 extern "C" size_t sgp_scratch_doubles(const sgp_model *m) {
     if (!m) return 0;
     if (lg_is_large(m->dev)) return 64;  // the large path keeps its state in the model workspace
-    return sgp_scratch_per_chain(m->dev.mp.ld, m->dev.mp.d, m->dev.mp.Dp);
+    return sgp_scratch_per_chain(m->dev.mp.ld, m->dev.mp.d, m->dev.mp.Dp, sgp_fields(m->dev.mp));
 }
 
 __global__ void k_phi_out(const double *phi, int ld, int N, int a0, int Dj, double *out) {

@@ -96,14 +96,14 @@ __host__ __device__ inline SmemPlan sgp_smem_plan(int d, int Dp, int nt, size_t 
     return s;
 }
 
-// per-chain scratch (doubles): per-sample fields, the 7 matrices, Jacobi log
-__host__ __device__ inline size_t sgp_scratch_mat_offset(int ld, int d, int Dp, int i) {
-    size_t off = (size_t)F_COUNT * ld;
+// per-chain scratch (doubles): per-sample fields (nf of them: sgp_fields), the 7 matrices, Jacobi log
+__host__ __device__ inline size_t sgp_scratch_mat_offset(int ld, int d, int Dp, int i, int nf) {
+    size_t off = (size_t)nf * ld;
     for (int k = 0; k < i; ++k) off += sgp_round2(sgp_mat_doubles(k, d, Dp));
     return off;
 }
-__host__ __device__ inline size_t sgp_scratch_per_chain(int ld, int d, int Dp) {
-    return sgp_scratch_mat_offset(ld, d, Dp, SGP_NMAT) + sgp_jacobi_log_doubles(d) + 2 * (size_t)d + 64;
+__host__ __device__ inline size_t sgp_scratch_per_chain(int ld, int d, int Dp, int nf) {
+    return sgp_scratch_mat_offset(ld, d, Dp, SGP_NMAT, nf) + sgp_jacobi_log_doubles(d) + 2 * (size_t)d + 64;
 }
 
 __device__ inline void setup_ws(ChainWS &w, EvalCtx &E, char *smem, const SmemPlan &pl, const ModelDev &M,
@@ -127,8 +127,8 @@ __device__ inline void setup_ws(ChainWS &w, EvalCtx &E, char *smem, const SmemPl
     double **mats[SGP_NMAT] = {&w.H, &E.wp, &w.W, &w.P[0], &w.P[1], &w.X, &w.T};
     for (int i = 0; i < SGP_NMAT; ++i)
         *mats[i] = pl.off_mat[i] != (size_t)-1 ? reinterpret_cast<double *>(smem + pl.off_mat[i])
-                                               : scratch + sgp_scratch_mat_offset(ld, d, Dp, i);
-    w.jlog = scratch + sgp_scratch_mat_offset(ld, d, Dp, SGP_NMAT);
+                                               : scratch + sgp_scratch_mat_offset(ld, d, Dp, i, sgp_fields(M.mp));
+    w.jlog = scratch + sgp_scratch_mat_offset(ld, d, Dp, SGP_NMAT, sgp_fields(M.mp));
     if (threadIdx.x == 0) *E.status = 0;
     __syncthreads();
 }

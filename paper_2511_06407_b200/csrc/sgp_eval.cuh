@@ -10,7 +10,7 @@ __host__ __device__ inline int sgp_trace_ks(int Dp, int CH, int nt) { return 2 *
 
 struct EvalCtx {
     ModelDev M;
-    double *S;      // per-sample fields, F_COUNT x ld (global scratch)
+    double *S;      // per-sample fields, sgp_fields(mp) x ld (global scratch)
     double *stage;  // smem staging of a chunk of samples (see stage_chunk_sm)
     double *wp;     // padded Dp x Dp copy of the contraction matrix
     int ext_trace;  // large-d path: 1 = c^(j) already in S; 2 = t[0, Dtot) already holds the likelihood part
@@ -37,12 +37,12 @@ __device__ __noinline__ double eval_lik(EvalCtx &E, const double *q) {
         if (i < N) {
             if (!isfinite(f0) || !isfinite(f1)) bad = true;
             E.S[F_F0 * ld + i] = f0;
-            E.S[F_F1 * ld + i] = f1;
+            if (mp.J == 2) E.S[F_F1 * ld + i] = f1;
             lik_sample(mp.lik, mp.vfloor, E.M.y[i], f0, f1, E.S, ld, i);
             su += E.S[F_U * ld + i];
         } else {
             // padding rows: zero weight everywhere
-            for (int k = 0; k < F_COUNT; ++k) E.S[k * ld + i] = 0.0;
+            for (int k = 0; k < sgp_fields(mp); ++k) E.S[k * ld + i] = 0.0;
         }
     }
     if (bad) set_status(E.status, SGP_STATUS_DIVERGENCE);
