@@ -549,9 +549,65 @@ __global__ void __launch_bounds__(DC_MT) k_dc_deflate(const DcMerge *mg, const d
         if (threadIdx.x == 0) zmax_s = zm;
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-        const double eps = 1.1102230246251565e-16;
-        const double tol = 8.0 * eps * fmax(fmax(fabs(key[0]), fabs(key[n - 1])), zmax_s);
+    const double eps = 1.1102230246251565e-16;
+    const double tol = 8.0 * eps * fmax(fmax(fabs(key[0]), fabs(key[n - 1])), zmax_s);
+    // Fast path (the common case): when no two neighbouring non-small poles are close, the
+    // sequential scan below keeps exactly the non-small entries and deflates the small ones,
+    // both in sorted order -- a block-wide compaction; the closeness test is the scan's own
+    // expression, so both paths decide identically.  Any close pair -> the sequential scan.
+    __shared__ int wsum[32], close_any;
+    {
+        const int per = (n + (int)blockDim.x - 1) / (int)blockDim.x;
+        const int t0 = min(n, (int)threadIdx.x * per), t1 = min(n, t0 + per);
+        int cnt = 0;
+        for (int t = t0; t < t1; ++t) cnt += !(rh * fabs(z[idx[t]]) <= tol);
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+        int incl = cnt;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += v;
+        }
+        if (lane == 31) wsum[warp] = incl;
+        if (threadIdx.x == 0) close_any = 0;
+        __syncthreads();
+        if (warp == 0) {
+            int w = lane < (int)(blockDim.x >> 5) ? wsum[lane] : 0;
+            for (int o = 1; o < 32; o <<= 1) {
+                const int v = __shfl_up_sync(0xffffffffu, w, o);
+                if (lane >= o) w += v;
+            }
+            wsum[lane] = w;  // inclusive over warps
+        }
+        __syncthreads();
+        int big_before = (warp ? wsum[warp - 1] : 0) + incl - cnt;
+        for (int t = t0; t < t1; ++t) {
+            const int jx = idx[t];
+            if (!(rh * fabs(z[jx]) <= tol))
+                kept[big_before++] = jx;
+            else
+                defl[t - big_before] = jx;
+        }
+        __syncthreads();
+        const int Kf = wsum[((blockDim.x >> 5) - 1)];
+        for (int i = 1 + threadIdx.x; i < Kf; i += blockDim.x) {
+            const int pj = kept[i - 1], jx = kept[i];
+            double sn = z[pj], c = z[jx];
+            const double tau = hypot(c, sn);
+            const double tt = dl[jx] - dl[pj];
+            c /= tau;
+            sn = -sn / tau;
+            if (fabs(tt * c * sn) <= tol) close_any = 1;
+        }
+        __syncthreads();
+        if (!close_any && threadIdx.x == 0) {
+            nk = Kf;
+            nd = n - Kf;
+            nr = 0;
+            kc[blockIdx.x] = Kf;
+            rhov[blockIdx.x] = rh;
+        }
+    }
+    if (close_any && threadIdx.x == 0) {
         int K = 0, M = 0, R = 0, pj = -1;
         for (int t = 0; t < n; ++t) {
             const int jx = idx[t];
